@@ -1,0 +1,232 @@
+"""Plain, slow, obviously-correct fp64 CPU oracle of the linear cross-entropy loss.
+
+TEST INFRASTRUCTURE ONLY -- imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference legs, never by the product path.
+
+What it computes (PAPER.md = P, SPEC.md = S, line numbers of /root/reference):
+
+* P:166 (Sec. 4.2, "Linear Cross-Entropy loss"): LinearCrossEntropyLoss "fuses
+  the final output projection with the cross-entropy computation, masks ignored
+  tokens before projection, and processes hidden states in chunks so that the
+  dense [B, S, V] tensor is never materialized".
+* P:132 (Sec. 3.3): LCE is a one-line drop-in for the standard CE, so its
+  result is by definition CE(H W^T, y).  S:279 states the same contract
+  ("match cross_entropy(hidden.W^T, targets)").
+
+LCE therefore reaches exactly (up to rounding order) a result with a plain
+definition, and this oracle IS that definition written out in fp64 (numpy,
+BLAS dgemm for the two products).  Chunking is a memory technique, not
+semantics (reading R7), so the oracle does not chunk.  It projects
+only the non-ignored rows (mask-first), which is also what makes
+garbage in ignored rows harmless.
+
+Readings of points the paper leaves open (full list in DESIGN.md):
+  R1 mean divides by N_v = #non-ignored rows
+  R2 N_v = 0 -> loss 0, grads 0
+  R3 ignore_index default -100; a label equal to it is ignored
+  R4 any other label outside [0, V) is an error
+  R5 lse / per-token loss of ignored rows are 0
+  R6 natural log
+  R11 upstream gradient g (dL/dloss) scales the gradients; default 1
+
+Every function is pinned in tests/test_oracle.py against closed forms, brute
+force, finite differences and torch's CPU fp64 cross-entropy + autograd.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+IGNORE_INDEX = -100  # S:498 "ignore_index = -100 -- conventional sentinel"
+
+__all__ = [
+    "IGNORE_INDEX",
+    "lce_forward",
+    "lce_backward",
+    "lce_rows",
+    "shard_stats",
+    "combine_shard_stats",
+]
+
+
+def _as_f64(a) -> np.ndarray:
+    """Exact widening of the inputs (bf16/fp32 values are exactly representable)."""
+    return np.asarray(a, dtype=np.float64)
+
+
+def _valid_rows(y: np.ndarray, vocab: int, ignore_index: int) -> np.ndarray:
+    """Step 1 ("masks ignored tokens"): V = {i : y_i != ignore_index}.
+
+    Labels outside [0, V) that are not ignore_index are an error.
+    """
+    y = np.asarray(y, dtype=np.int64)
+    valid = y != ignore_index
+    bad = valid & ((y < 0) | (y >= vocab))
+    if bad.any():
+        i = int(np.flatnonzero(bad)[0])
+        raise ValueError(f"label {int(y[i])} at row {i} outside [0, {vocab})")
+    return valid
+
+
+def _scale(reduction: str, n_valid: int, grad_loss: float) -> float:
+    """c = g (sum) or g / N_v (mean); 0 if N_v = 0."""
+    if reduction not in ("mean", "sum"):
+        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+    if n_valid == 0:
+        return 0.0
+    return float(grad_loss) / n_valid if reduction == "mean" else float(grad_loss)
+
+
+def _log_softmax_stats(z: np.ndarray):
+    """Per-row m = max_j z_ij and lse_i = m_i + ln sum_j exp(z_ij - m_i)."""
+    m = z.max(axis=1)
+    lse = m + np.log(np.exp(z - m[:, None]).sum(axis=1))
+    return m, lse
+
+
+def lce_forward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
+                reduction: str = "mean") -> dict:
+    """Loss, per-token lse and per-token loss of CE(H W^T, y), mask-first.
+
+    hidden [N, D], weight [V, D], labels [N] ints.  Returns a dict with
+    ``loss`` (float), ``lse`` [N] (0 on ignored rows), ``token_loss`` [N]
+    (0 on ignored rows) and ``n_valid`` (int).
+    """
+    H = _as_f64(hidden)
+    W = _as_f64(weight)
+    y = np.asarray(labels, dtype=np.int64)
+    N, V = H.shape[0], W.shape[0]
+    valid = _valid_rows(y, V, ignore_index)           # step 1
+    rows = np.flatnonzero(valid)
+    n_valid = int(rows.size)
+    lse = np.zeros(N)
+    tok = np.zeros(N)
+    if n_valid:
+        z = H[rows] @ W.T                             # step 2: logits of valid rows only
+        _, lse_v = _log_softmax_stats(z)              # step 3
+        z_t = z[np.arange(n_valid), y[rows]]
+        lse[rows] = lse_v
+        tok[rows] = lse_v - z_t                       # step 4: NLL of log-softmax
+    total = float(tok.sum())                          # step 5
+    if reduction == "mean":
+        loss = total / n_valid if n_valid else 0.0    # R1, R2
+    elif reduction == "sum":
+        loss = total
+    else:
+        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+    return {"loss": loss, "lse": lse, "token_loss": tok, "n_valid": n_valid}
+
+
+def lce_backward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
+                 reduction: str = "mean", grad_loss: float = 1.0) -> dict:
+    """Analytic gradients of the loss: dH = G W, dW = G^T H.
+
+    G_ij = c (softmax(z_i)_j - [j = y_i]) for valid rows, 0 for ignored rows,
+    with c from ``_scale``.  Returns ``dH`` [N, D], ``dW`` [V, D] (fp64),
+    ``n_valid`` and ``c``.
+    """
+    H = _as_f64(hidden)
+    W = _as_f64(weight)
+    y = np.asarray(labels, dtype=np.int64)
+    N, V = H.shape[0], W.shape[0]
+    valid = _valid_rows(y, V, ignore_index)
+    rows = np.flatnonzero(valid)
+    n_valid = int(rows.size)
+    c = _scale(reduction, n_valid, grad_loss)          # step 7
+    dH = np.zeros_like(H)
+    dW = np.zeros_like(W)
+    if n_valid:
+        Hv = H[rows]
+        z = Hv @ W.T
+        _, lse = _log_softmax_stats(z)
+        G = np.exp(z - lse[:, None])                   # step 8: p_ij
+        G[np.arange(n_valid), y[rows]] -= 1.0          #         p - onehot
+        G *= c
+        dH[rows] = G @ W                               # step 9
+        dW = G.T @ Hv
+    return {"dH": dH, "dW": dW, "n_valid": n_valid, "c": c}
+
+
+def lce_rows(hidden, weight, labels, rows, n_valid: int,
+             ignore_index: int = IGNORE_INDEX, reduction: str = "mean",
+             grad_loss: float = 1.0) -> dict:
+    """Row-local quantities for selected rows only (lse, token loss, dH rows).
+
+    Used to check the GPU at sizes where the full oracle is too slow: lse_i,
+    l_i and dH_i depend only on row i, W, and (for dH) the scalar c, which
+    needs the global ``n_valid``.  Ignored rows give 0.
+    """
+    W = _as_f64(weight)
+    rows = np.asarray(rows, dtype=np.int64)
+    H = _as_f64(np.asarray(hidden)[rows])
+    y = np.asarray(labels, dtype=np.int64)[rows]
+    V = W.shape[0]
+    valid = _valid_rows(y, V, ignore_index)
+    c = _scale(reduction, n_valid, grad_loss)
+    k = rows.size
+    lse = np.zeros(k)
+    tok = np.zeros(k)
+    dH = np.zeros((k, W.shape[1]))
+    sel = np.flatnonzero(valid)
+    if sel.size:
+        z = H[sel] @ W.T
+        _, l = _log_softmax_stats(z)
+        lse[sel] = l
+        tok[sel] = l - z[np.arange(sel.size), y[sel]]
+        G = np.exp(z - l[:, None])
+        G[np.arange(sel.size), y[sel]] -= 1.0
+        dH[sel] = c * (G @ W)
+    return {"lse": lse, "token_loss": tok, "dH": dH}
+
+
+def shard_stats(hidden, weight_shard, labels, vocab_start: int, vocab_total: int,
+                ignore_index: int = IGNORE_INDEX) -> dict:
+    """Per-row statistics of one vocab shard (loss-parallel).
+
+    P:180: the output projection is sharded "over the vocab dimension across
+    the tensor parallelism mesh".  Shard r holds rows [vocab_start,
+    vocab_start + V_r) of W and computes, for each valid row i, the partial
+    max m_ir, sum-exp s_ir = sum_{j in shard} exp(z_ij - m_ir) and the target
+    logit z_{i,y_i} if y_i is in the shard (else 0).  Ignored rows give
+    (m, s, z) = (-inf, 0, 0).
+    """
+    H = _as_f64(hidden)
+    Wr = _as_f64(weight_shard)
+    y = np.asarray(labels, dtype=np.int64)
+    N = H.shape[0]
+    valid = _valid_rows(y, vocab_total, ignore_index)
+    rows = np.flatnonzero(valid)
+    m = np.full(N, -np.inf)
+    s = np.zeros(N)
+    zt = np.zeros(N)
+    if rows.size:
+        z = H[rows] @ Wr.T
+        mr = z.max(axis=1)
+        m[rows] = mr
+        s[rows] = np.exp(z - mr[:, None]).sum(axis=1)
+        local = y[rows] - vocab_start
+        own = (local >= 0) & (local < Wr.shape[0])
+        zt[rows[own]] = z[np.flatnonzero(own), local[own]]
+    return {"m": m, "s": s, "z_target": zt, "valid": valid}
+
+
+def combine_shard_stats(stats: list) -> dict:
+    """Merge shard statistics into the global lse and per-token loss.
+
+    M_i = max_r m_ir;  lse_i = M_i + ln sum_r s_ir exp(m_ir - M_i);
+    z_{i,y_i} = sum_r z_ir (exactly one shard owns the label);
+    l_i = lse_i - z_{i,y_i}.  Ignored rows (all m = -inf) give 0.
+    """
+    m = np.stack([st["m"] for st in stats])
+    s = np.stack([st["s"] for st in stats])
+    zt = np.stack([st["z_target"] for st in stats]).sum(axis=0)
+    valid = stats[0]["valid"]
+    M = m.max(axis=0)
+    lse = np.zeros(m.shape[1])
+    tok = np.zeros(m.shape[1])
+    v = np.flatnonzero(valid)
+    if v.size:
+        w = s[:, v] * np.exp(m[:, v] - M[v])
+        lse[v] = M[v] + np.log(w.sum(axis=0))
+        tok[v] = lse[v] - zt[v]
+    return {"lse": lse, "token_loss": tok}
