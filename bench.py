@@ -1,0 +1,345 @@
+"""LCE fwd+bwd benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama8b] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (vocab-parallel, NCCL)
+
+A step is one pass of the whole hot path: lce_forward +
+lce_backward on one synthetic batch already resident in HBM.  value =
+non-ignored tokens per second of the whole job (all ranks cooperate on one
+batch: vocab-parallel strong scaling).  The inputs (W is 1.05 GB at the 8B
+head shape) are larger than the 126 MB L2, so no explicit flush is needed.
+`--impl reference` times the fp64 CPU oracle (the only reference this tier
+has) on a bounded row sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth.inputs import CONFIGS, IGNORE, make_config  # noqa: E402
+
+METRIC = "LCE fwd+bwd tokens/sec and % bf16 tensor peak at 1/2/4/8 B200; peak HBM bytes"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops_sustained", 1383.0), d.get("bf16_tflops", 1638.5), d.get("hbm_gbs", 6545.3), "measured"
+    return 1400.0, 1590.0, 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.05)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                rows.append(f)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        smax = max(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        loaded = [x for x in sm if x > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
+
+
+def oracle_sample(cfg_name: str, n_rows: int, seed: int = 0):
+    """Rows of the same workload for the CPU oracle (exact bf16 values)."""
+    from synth.inputs import make_inputs, make_labels
+
+    c = CONFIGS[cfg_name]
+    y = make_labels(c["N"], c["V"], c["labels"], c["ignore_frac"], 3000 + c["k"])
+    rng = np.random.default_rng(seed)
+    rows = np.sort(rng.choice(c["N"], size=min(n_rows, c["N"]), replace=False))
+    inp = make_inputs(len(rows), c["D"], c["V"], k=c["k"], device="cpu", label_override=y[rows])
+    return inp.hidden.float().numpy(), inp.weight.float().numpy(), inp.labels.numpy()
+
+
+def run_oracle_step(H, W, y):
+    from oracle import lce_backward, lce_forward
+
+    f = lce_forward(H, W, y)
+    lce_backward(H, W, y)
+    return f["n_valid"]
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def time_oracle(cfg_name: str, target_s: float = 12.0):
+    """Oracle fwd+bwd on a bounded row sample; returns (tokens/s, rows, seconds)."""
+    H, W, y = oracle_sample(cfg_name, 4)
+    t0 = time.perf_counter()
+    run_oracle_step(H, W, y)
+    t_small = time.perf_counter() - t0
+    # the dW GEMM (V x D output) has a fixed cost; scale rows on the per-row slope
+    H2, W2, y2 = oracle_sample(cfg_name, 16)
+    t0 = time.perf_counter()
+    run_oracle_step(H2, W2, y2)
+    t16 = time.perf_counter() - t0
+    per_row = max((t16 - t_small) / 12, 1e-4)
+    n = int(max(8, min(CONFIGS[cfg_name]["N"], (target_s - t_small) / per_row)))
+    H3, W3, y3 = oracle_sample(cfg_name, n)
+    t0 = time.perf_counter()
+    nv = run_oracle_step(H3, W3, y3)
+    dt = time.perf_counter() - t0
+    return nv / dt, n, nv, dt
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    c = CONFIGS[args.config]
+    _, n, nv, dt = time_oracle(args.config, target_s=8.0)
+    H, W, y = oracle_sample(args.config, n)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        run_oracle_step(H, W, y)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        nv = run_oracle_step(H, W, y)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    v = nv / t
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload_name(args.config), "N": c["N"], "D": c["D"], "V": c["V"]},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{n} of {c['N']} rows ({nv} valid), full D={c['D']}, V={c['V']}, fwd+bwd fp64 per step"},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(cfg):
+    c = CONFIGS[cfg]
+    tag = {"llama1b": "Llama-3.2-1B head", "llama8b": "Llama-3.1-8B head", "qwen7b": "Qwen2.5-7B head packed",
+           "llama70b": "Llama-3.1-70B head", "tiny": "tiny"}[cfg]
+    return f"{tag}: N={c['N']} D={c['D']} V={c['V']}"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="llama8b", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        return reference_arm(args, rank)
+
+    import paper_2605_21442_b200 as F
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    comm = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        comm = F.Comm.from_process_group()
+    c = CONFIGS[args.config]
+    inp = make_config(args.config, device=dev)
+    N, D, V = c["N"], c["D"], c["V"]
+    vstart, vl = F.shard_range(V, world, rank) if world > 1 else (0, V)
+    W = inp.weight[vstart:vstart + vl].contiguous()
+    del inp.weight
+    H, y = inp.hidden, inp.labels
+    nv = int((y != IGNORE).sum().item())
+    ws = F.Workspace()
+    stream = torch.cuda.current_stream()
+    out = {
+        "loss": torch.empty(1, dtype=torch.float32, device=dev), "lse": torch.empty(N, dtype=torch.float32, device=dev),
+        "n_valid": torch.empty(1, dtype=torch.int32, device=dev), "token_loss": None,
+    }
+    dH = torch.empty_like(H)
+    dW = torch.empty(vl, D, dtype=torch.float32, device=dev)
+
+    def step():
+        F.forward(H, W, y, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out)
+        F.backward(H, W, y, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH, dweight=dW,
+                   workspace=ws)
+
+    torch.cuda.reset_peak_memory_stats(dev)
+    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    F.profile_enable(True)
+    l0 = F.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = F.launch_count() - l0
+    prof = F.profile_read()
+    F.profile_enable(False)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        if dist:
+            dist.barrier()
+    peak_hbm = torch.cuda.max_memory_allocated(dev)
+    ms_step = ms / args.steps
+    value = nv * args.steps / (ms / 1e3)
+    sus, burst, hbm, src = peaks()
+    flops_step = 8.0 * nv * V * D
+    tensor_frac = flops_step / (ms_step / 1e3) / (sus * 1e12 * world)
+
+    # dominant kernel (by device time inside the timed region, on the launching stream)
+    gemm_flops = {"fwd_gemm": 2.0 * nv * vl * D, "bwd_g": 2.0 * nv * vl * D, "bwd_dh": 2.0 * nv * vl * D,
+                  "bwd_dw": 2.0 * nv * vl * D}
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in prof.items()
+               if v[1]}
+    roof = None
+    if dom in gemm_flops and dom_n:
+        per_launch_flops = gemm_flops[dom] * args.steps / dom_n
+        achieved = per_launch_flops / (dom_ms / dom_n / 1e3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s", "frac": achieved / sus,
+                "traffic": traffic, "kernel": dom, "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+                "flops_per_launch": per_launch_flops,
+                "share_of_step": dom_ms / ms if world == 1 else None}
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Hh = H.cpu().pin_memory()
+        Wh = W.cpu().pin_memory()
+        yh = y.cpu().pin_memory()
+        lossh = torch.empty(1, dtype=torch.float32).pin_memory()
+        Hd, Wd, yd = torch.empty_like(H), torch.empty_like(W), torch.empty_like(y)
+
+        def e2e_step():
+            Hd.copy_(Hh, non_blocking=True)
+            Wd.copy_(Wh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            F.forward(Hd, Wd, yd, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out)
+            F.backward(Hd, Wd, yd, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH, dweight=dW,
+                       workspace=ws)
+            lossh.copy_(out["loss"], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        if dist:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": nv * args.steps / (ems / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": H.numel() * 2 + W.numel() * 2 + y.numel() * 4, "d2h_bytes_per_step": 4,
+               "ms_per_step": ems / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v_cpu, n_rows, nv_rows, dt = time_oracle(args.config)
+        cpu = {"value": v_cpu, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+               "sample": f"{n_rows} of {N} rows ({nv_rows} valid), full D={D}, V={V}, one fp64 fwd+bwd in {dt:.1f}s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_name(args.config), "N": N, "N_valid": nv, "D": D, "V": V,
+                       "parallelism": f"vocab-parallel x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (W alone is %.2f GB > 126 MB); no flush" % (V * D * 2 / 1e9)},
+            "tensor_frac": tensor_frac, "tensor_frac_note": f"8*N_v*V*D per step / (time x {src} sustained bf16 peak x GPUs)",
+            "peak_hbm_bytes": peak_hbm, "naive_logits_bytes_fp32": N * V * 4,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+            "clocks": clk, "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * lce.h -- C ABI of the B200 (sm_100a) linear cross-entropy library (liblce.so).
+ *
+ * What it computes (PAPER.md = P, /root/reference line numbers):
+ *   P:166 (Sec. 4.2 "Linear Cross-Entropy loss"): the loss "fuses the final
+ *   output projection with the cross-entropy computation, masks ignored tokens
+ *   before projection, and processes hidden states in chunks so that the dense
+ *   [B, S, V] tensor is never materialized".  P:132 (Sec. 3.3): it is a drop-in
+ *   for the standard CE, i.e. loss = CE(H W^T, y) with ignore_index.
+ *   P:169 / P:180 (Sec. 5): under tensor parallelism the output projection is
+ *   sharded over the vocabulary ("loss parallel"); see lce_comm_* below.
+ *
+ * Notation: H = hidden [N, D] bf16, W = weight [V_l, D] bf16 (this rank's
+ * vocab rows), y = labels [N] int32, N_v = #{i : y_i != ignore_index},
+ * lse_i = ln sum_j exp(z_ij) with z = H W^T (natural log, fp32),
+ * loss_i = lse_i - z_{i, y_i}, L = sum_i loss_i (SUM) or sum_i loss_i / N_v
+ * (MEAN; 0 when N_v = 0).  Gradients: G_ij = c (softmax(z_i)_j - [j = y_i]),
+ * c = g (SUM) or g / N_v (MEAN), dH = G W, dW = G^T H.
+ *
+ * Conventions for every entry point:
+ *  - All tensor pointers are DEVICE pointers unless stated otherwise; all
+ *    tensors are dense row-major.  bf16 values are passed as uint16_t bit
+ *    patterns.  Every pointer must be 16-byte aligned.
+ *  - The caller owns every buffer.  The library never allocates or frees
+ *    device memory (the only exception is NCCL state inside an lce_comm_t),
+ *    keeps no pointer after return, and never synchronises the stream except
+ *    in lce_check_device_status.  All work is enqueued on `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *  - Host-detectable errors return before anything is enqueued and leave all
+ *    outputs untouched.  CUDA launch errors return LCE_ERR_CUDA.
+ *  - Results do not depend on the chunk budget beyond fp32 rounding order.
+ *  - Calls on different streams with different workspaces are independent.
+ */
+#ifndef LCE_H_
+#define LCE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LCE_ABI_VERSION 1
+
+typedef enum {
+  LCE_OK = 0,
+  LCE_ERR_NULL = 1,        /* required pointer is NULL                         */
+  LCE_ERR_SHAPE = 2,       /* N<0, D<=0, D%8!=0, V_l<=0, bad vocab range, >2^31 */
+  LCE_ERR_ALIGN = 3,       /* a pointer is not 16-byte aligned                 */
+  LCE_ERR_REDUCTION = 4,   /* reduction is not LCE_MEAN / LCE_SUM              */
+  LCE_ERR_WORKSPACE = 5,   /* workspace_bytes < lce_workspace_bytes(problem)   */
+  LCE_ERR_LABEL_RANGE = 6, /* a label outside [0, V_total) that is not ignored */
+  LCE_ERR_DEVICE = 7,      /* current device is not sm_100 (B200)              */
+  LCE_ERR_CUDA = 8,        /* a CUDA runtime / driver call failed              */
+  LCE_ERR_NCCL = 9,        /* NCCL missing or an NCCL call failed              */
+  LCE_ERR_COMM = 10        /* communicator does not match the problem          */
+} lce_status_t;
+
+typedef enum { LCE_MEAN = 0, LCE_SUM = 1 } lce_reduction_t;
+
+/* Opaque vocab-parallel communicator (NCCL over NVLink).  NULL = one GPU. */
+typedef struct lce_comm_s* lce_comm_t;
+
+typedef struct {
+  int64_t n_tokens;      /* N >= 0                                                  */
+  int64_t hidden_dim;    /* D > 0, D % 8 == 0 (16-byte TMA row pitch)               */
+  int64_t vocab_local;   /* V_l > 0: rows of `weight` on this rank (= V if 1 GPU)   */
+  int64_t vocab_start;   /* global id of local weight row 0 (0 on one GPU)          */
+  int64_t vocab_total;   /* V: labels must lie in [0, V) unless ignored             */
+  int32_t ignore_index;  /* rows with this label are dropped before projection      */
+  int32_t reduction;     /* lce_reduction_t                                         */
+  int64_t chunk_budget_bytes; /* bytes for one bf16 G chunk in the backward; 0 =
+                                 default (512 MiB).  A performance knob only.       */
+} lce_problem_t;
+
+/* Bytes of caller-provided device workspace both lce_forward and lce_backward
+ * need for `p` (same value for both).  Pure host function.  Returns 0 if `p`
+ * is invalid.  Upper bound is O(N*D + N*V_l/128 + budget) -- never N*V_l. */
+size_t lce_workspace_bytes(const lce_problem_t* p);
+
+/* Forward: mask-first compaction, z = H W^T tile by tile on the tensor cores
+ * (tcgen05, fp32 accumulation in TMEM), online logsumexp + target pick in the
+ * epilogue, fixed-order combine.  The N x V_l logits never exist in memory.
+ *   hidden     [N, D]   bf16, row i = token i
+ *   weight     [V_l, D] bf16, row j = vocab id vocab_start + j
+ *   labels     [N]      int32 global vocab ids or ignore_index
+ *   loss       [1] fp32 out: L (NaN if a label was out of range, see below)
+ *   lse        [N] fp32 out: lse_i; 0 for ignored rows
+ *   token_loss [N] fp32 out or NULL: loss_i; 0 for ignored rows
+ *   n_valid    [1] int32 out or NULL: N_v
+ *   workspace  device scratch of >= lce_workspace_bytes(p) bytes
+ * A label outside [0, V) that is not ignore_index excludes its row from all
+ * compute, sets a bit in the workspace status word and makes `loss`
+ * NaN (no host sync needed); lce_check_device_status then returns
+ * LCE_ERR_LABEL_RANGE.  With comm != NULL every rank passes identical
+ * hidden/labels and its own weight shard; loss/lse are then global and
+ * bitwise identical on all ranks. */
+lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm,
+                         const uint16_t* hidden, const uint16_t* weight,
+                         const int32_t* labels, float* loss, float* lse,
+                         float* token_loss, int32_t* n_valid,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Backward: recomputes z tile by tile (same tiling as the forward), forms
+ * G = softmax - onehot from the saved lse in the epilogue (bf16 RNE, one
+ * bounded vocab chunk at a time), then dH += G_c W_c and dW_c = G_c^T H on
+ * the tensor cores with fp32 accumulation.
+ *   lse        [N] fp32 in: the forward's lse output (same H, W, labels)
+ *   grad_loss  [1] fp32 in (device) or NULL for 1.0: g = dL_total/dL
+ *   dhidden    [N, D] bf16 out: dH (RNE from fp32); rows of ignored tokens 0
+ *   dweight    [V_l, D] fp32 out: dW for this rank's rows
+ *   accumulate_dweight  0: dweight = dW, 1: dweight += dW
+ * With comm != NULL, dH is summed over ranks (NCCL all-reduce) and is the
+ * same on all ranks; dweight is the local shard (concatenate in rank order). */
+lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm,
+                          const uint16_t* hidden, const uint16_t* weight,
+                          const int32_t* labels, const float* lse,
+                          const float* grad_loss, uint16_t* dhidden,
+                          float* dweight, int accumulate_dweight,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* Synchronises `stream`, reads the status word of `workspace` and returns
+ * LCE_ERR_LABEL_RANGE if the most recent lce_forward / lce_backward that used
+ * this workspace saw a bad label, LCE_OK otherwise.  Every call rewrites the
+ * status word, so a fresh (uninitialised) workspace needs no clearing. */
+lce_status_t lce_check_device_status(void* workspace, void* stream);
+
+/* ---- vocab-parallel communicator (P:180 loss parallel) --------------------
+ * Rank 0 creates a 128-byte id (host memory) and distributes it out of band
+ * (the Python binding uses torch.distributed.broadcast_object_list); every
+ * rank then calls lce_comm_init with its own CUDA device current.  NCCL is
+ * loaded at run time (libnccl.so.2); LCE_ERR_NCCL if unavailable. */
+lce_status_t lce_comm_get_unique_id(uint8_t id[128]);
+lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank);
+lce_status_t lce_comm_destroy(lce_comm_t comm);
+int lce_comm_size(lce_comm_t comm);
+int lce_comm_rank(lce_comm_t comm);
+
+/* ---- introspection ------------------------------------------------------- */
+const char* lce_status_string(lce_status_t s);
+int lce_abi_version(void);
+/* Total number of CUDA kernels this library has launched since load. */
+uint64_t lce_launch_count(void);
+
+/* Kernel classes for the profiler below. */
+typedef enum {
+  LCE_K_PREP = 0,     /* S0 label scan + stable compaction          */
+  LCE_K_GATHER = 1,   /* S0 gather of valid rows of H (+ lse rows)  */
+  LCE_K_FWD = 2,      /* S1+S2 forward GEMM + online-LSE epilogue   */
+  LCE_K_COMBINE = 3,  /* S3 merge of per-tile partials, loss        */
+  LCE_K_BWD_G = 4,    /* S4 recompute GEMM + G epilogue             */
+  LCE_K_BWD_DH = 5,   /* S6 dH GEMM                                 */
+  LCE_K_BWD_DW = 6,   /* S5 dW GEMM                                 */
+  LCE_K_FINAL = 7,    /* S7 dH cast/scatter (multi-GPU)             */
+  LCE_K_COMM = 8,     /* NCCL collectives                           */
+  LCE_K_COUNT = 9
+} lce_kernel_class_t;
+
+/* Opt-in per-kernel timing: while enabled, every launch is bracketed by CUDA
+ * events on the launching stream (no extra synchronisation).  lce_profile_read
+ * synchronises the recorded events and returns, per lce_kernel_class_t, the
+ * summed device milliseconds and launch counts since lce_profile_enable(1);
+ * it then clears the record.  Host-thread-global; not for concurrent use. */
+lce_status_t lce_profile_enable(int on);
+lce_status_t lce_profile_read(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT]);
+
+/* ---- diagnostics (tests only) ---------------------------------------------
+ * C[M, N] (fp32, row-major, ldc = N) = A * B^T through the same tcgen05 GEMM
+ * mainloop the loss kernels use.  a_mn = 0: A stored [M, K] (K-major);
+ * a_mn = 1: A stored [K, M] (M-major).  b_mn = 0: B stored [N, K];
+ * b_mn = 1: B stored [K, N].  M, N, K > 0; leading dims are the stored row
+ * lengths and must be multiples of 8. */
+lce_status_t lce_debug_gemm(const uint16_t* A, const uint16_t* B, float* C,
+                            int64_t M, int64_t N, int64_t K, int a_mn, int b_mn,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LCE_H_ */

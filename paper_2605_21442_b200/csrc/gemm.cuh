@@ -1,0 +1,225 @@
+// gemm.cuh -- persistent, warp-specialised tcgen05 GEMM mainloop for sm_100a.
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]      (bf16 x bf16 -> fp32 in TMEM)
+//
+// Every GEMM on the LCE hot path runs through
+// this one mainloop; they differ only in operand major-ness (A_MN / B_MN) and in
+// the epilogue policy `Epi`, which consumes the fp32 accumulator straight from
+// TMEM, so no GEMM result (in particular no logit tile) is ever written to HBM
+// unless the epilogue chooses to.
+//
+// CTA layout (256 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer (one elected lane): A/B k-blocks -> smem ring
+//   warp 1      MMA issuer (one lane): tcgen05.mma 128x256x16, fp32 accum in TMEM
+//   warp 2      TMEM allocator (512 columns = 2 accumulator buffers of 256)
+//   warps 4..7  epilogue: tcgen05.ld the accumulator (thread = one tile row =
+//               one TMEM lane) while the MMA warp fills the other buffer.
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA, kStages deep) and TMEM
+// full/empty mbarriers (MMA <-> epilogue, 2 deep).
+#pragma once
+
+#include "sm100.cuh"
+
+namespace lce {
+
+constexpr int BM = 128;     // tile rows   (TMEM lanes)
+constexpr int BN = 256;     // tile cols   (TMEM columns per accumulator buffer)
+constexpr int BK = 64;      // k-block: 64 bf16 = one 128-byte swizzle row
+constexpr int UK = 16;      // K of one tcgen05.mma.kind::f16
+constexpr int kStages = 4;  // smem ring depth (4 x 48 KB)
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+constexpr int kGroupM = 16;  // raster: 16 m-blocks share each n-block sweep (L2 reuse)
+
+constexpr int kAStageBytes = BM * BK * 2;  // 16 KB
+constexpr int kBStageBytes = BN * BK * 2;  // 32 KB
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*align slack*/ + 256 /*barriers*/;
+
+// Problem extents.  M and K may live on the device (they depend on the number
+// of non-ignored tokens, which the host never reads back).
+struct GemmDims {
+  const int32_t* m_dev;
+  int32_t m_static;
+  const int32_t* k_dev;
+  int32_t k_static;
+  int32_t n;
+};
+
+// Geometry handed to the epilogue for one output tile.
+struct TileInfo {
+  int m0, n0, n_blk;
+  int M, N;
+  int row;        // row of this thread inside the tile (== TMEM lane)
+  bool zero_acc;  // K == 0: the accumulator was never written, treat as 0
+};
+
+__device__ __forceinline__ int dev_or(const int32_t* p, int32_t v) { return p ? *p : v; }
+
+__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
+  const int per_group = kGroupM * num_n;
+  const int g = t / per_group;
+  const int first_m = g * kGroupM;
+  const int gsz = min(num_m - first_m, kGroupM);
+  const int r = t - g * per_group;
+  m_blk = first_m + r % gsz;
+  n_blk = r / gsz;
+}
+
+template <bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmDims dims, const typename Epi::Params ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kStages * kAStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int M = dev_or(dims.m_dev, dims.m_static);
+  const int K = dev_or(dims.k_dev, dims.k_static);
+  const int N = dims.n;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_k = (K + BK - 1) / BK;
+  const int num_tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && num_k > 0) {
+      // ---------------------------------------------------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_of(t, num_m, num_n, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], kAStageBytes + kBStageBytes);
+          uint8_t* a = sA + stage * kAStageBytes;
+          uint8_t* b = sB + stage * kBStageBytes;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d(a, &tmA, &full[stage], k0, m0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * BK * 128, &tmA, &full[stage], m0 + 64 * j, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d(b, &tmB, &full[stage], k0, n0);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * BK * 128, &tmB, &full[stage], n0 + 64 * j, k0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * kAStageBytes);
+          const uint32_t b_addr = smem_u32(sB + stage * kBStageBytes);
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + kk * (UK * 128), BK * 128, 1024)
+                                     : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
+                                     : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
+            mma_bf16_ss(d, ad, bd, idesc, (kb | kk) != 0);
+          }
+          mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (num_k > 0) {
+          mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        } else {
+          mbar_arrive(&tfull[acc]);
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_of(t, num_m, num_n, mb, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      TileInfo ti{mb * BM, nb * BN, nb, M, N, q * 32 + lane, num_k == 0};
+      Epi::apply(ep, taddr, ti);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
+}
+
+// Loads the 32-column chunk `c` of this thread's accumulator row as floats.
+__device__ __forceinline__ void load_chunk(uint32_t taddr, int c, bool zero, float (&x)[32]) {
+  uint32_t v[32];
+  tmem_ld32(taddr + c * 32, v);
+  tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = zero ? 0.f : __uint_as_float(v[j]);
+}
+
+}  // namespace lce

@@ -1,0 +1,476 @@
+// kernels.cuh -- LCE-specific epilogues for the tcgen05 mainloop and the small
+// HBM-bound kernels around it.
+#pragma once
+
+#include <math.h>
+
+#include "gemm.cuh"
+
+namespace lce {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr uint32_t kStatusBadLabel = 1u;
+
+// Device-side header at the start of the workspace.
+struct Header {
+  uint32_t status;    // error bits of the most recent call (kStatusBadLabel)
+  int32_t n_valid;    // N_v of the last prep
+  float c;            // gradient scale: g (sum) or g / N_v (mean), 0 if N_v = 0
+  uint32_t counter;   // last-block-done counter for deterministic reductions
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // RNE
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ============================================================ S1+S2 forward epilogue
+// Per row of the 128x256 logit tile (still in TMEM): running max m and
+// sum-exp s relative to m over the tile's valid columns (cols >= n_cols are
+// -inf), and the target logit if the row's label falls in this tile.
+// Writes the partials (m, s) of tile column n_blk; the logits never leave
+// the SM.  (the dense [B,S,V] tensor is never materialised.)
+struct EpiLse {
+  struct Params {
+    const int32_t* yc;    // [N_v] compacted labels (global vocab ids)
+    int32_t label_off;    // global vocab id of GEMM column 0
+    int32_t n_cols;       // valid GEMM columns (V_l)
+    float* part_m;        // [n_tiles][ld]
+    float* part_s;        // [n_tiles][ld]
+    int64_t ld;
+    float* zt;            // [N_v] target logit (single writer: the owning tile)
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+    const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;  // tile-relative target column
+    float m = -INFINITY, s = 0.f, zt = 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      const int cb = t.n0 + c * 32;
+      if (cb + 32 > p.n_cols) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (cb + j >= p.n_cols) x[j] = -INFINITY;
+      }
+      if ((yl >> 5) == c) {
+        const int jt = yl & 31;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j == jt) zt = x[j];
+      }
+      float cm = x[0];
+#pragma unroll
+      for (int j = 1; j < 32; ++j) cm = fmaxf(cm, x[j]);
+      const float mn = fmaxf(m, cm);
+      if (mn == -INFINITY) continue;  // whole chunk masked and nothing before it
+      const float mnl = mn * kLog2e;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        a0 += ex2_approx(fmaf(x[j + 0], kLog2e, -mnl));
+        a1 += ex2_approx(fmaf(x[j + 1], kLog2e, -mnl));
+        a2 += ex2_approx(fmaf(x[j + 2], kLog2e, -mnl));
+        a3 += ex2_approx(fmaf(x[j + 3], kLog2e, -mnl));
+      }
+      const float cs = (a0 + a1) + (a2 + a3);
+      s = (m == -INFINITY) ? cs : fmaf(s, ex2_approx((m - mn) * kLog2e), cs);
+      m = mn;
+    }
+    if (valid) {
+      p.part_m[t.n_blk * p.ld + r] = m;
+      p.part_s[t.n_blk * p.ld + r] = s;
+      if (yl >= 0 && yl < BN && t.n0 + yl < p.n_cols) p.zt[r] = zt;
+    }
+  }
+};
+
+// ============================================================ S4 backward G epilogue
+// Recomputed logit tile -> G = exp(z - lse) - [j == y] (unscaled, A9), bf16
+// RNE, into the vocab chunk buffer G_c[row, col].  Rows >= N_v and columns
+// >= n_cols are written as exact zeros so the next two GEMMs can run over
+// whole k-blocks.
+struct EpiG {
+  struct Params {
+    const int32_t* yc;
+    const float* lse_c;   // [N_v] lse of compacted rows
+    int32_t label_off;    // global vocab id of chunk column 0
+    int32_t n_cols;       // valid columns of this chunk
+    uint16_t* G;          // [rows_cap][ldg] bf16
+    int64_t ldg;
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+    const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;
+    const float lsel = valid ? p.lse_c[r] * kLog2e : 0.f;
+    uint4* dst = reinterpret_cast<uint4*>(p.G + static_cast<int64_t>(r) * p.ldg + t.n0);
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      const int cb = t.n0 + c * 32;
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c * 32 + j == yl ? 1.f : 0.f);
+        float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c * 32 + j + 1 == yl ? 1.f : 0.f);
+        if (!valid || cb + j >= p.n_cols) g0 = 0.f;
+        if (!valid || cb + j + 1 >= p.n_cols) g1 = 0.f;
+        w[j / 2] = pack_bf16x2(g0, g1);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) dst[c * 4 + v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+    }
+  }
+};
+
+// ============================================================ S6 dH epilogue
+// acc = (G_c W_c)[row, cols] for vocab chunk k.  Chunks are summed unscaled
+// in fp32 (acc_buf); on the last chunk (single GPU) the sum is scaled by c,
+// rounded to bf16 and scattered to dhidden[idx[row]] directly.
+struct EpiDH {
+  struct Params {
+    float* acc_buf;        // [rows_cap][ld] fp32 running sum over chunks
+    int64_t ld;            // D
+    int32_t first;         // first chunk: overwrite acc_buf
+    int32_t last_direct;   // last chunk and no cross-rank reduction: write dhidden
+    const Header* hdr;     // c
+    uint16_t* dhidden;     // [N][D] bf16
+    const int32_t* idx;    // compact row -> token row
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+    const float cs = p.last_direct ? p.hdr->c : 1.f;
+    float* accrow = p.acc_buf + static_cast<int64_t>(r) * p.ld;
+    uint16_t* orow = nullptr;
+    if (valid && p.last_direct) orow = p.dhidden + static_cast<int64_t>(p.idx[r]) * p.ld;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      const int cb = t.n0 + c * 32;
+      if (!valid) continue;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int col = cb + 4 * v;
+        if (col >= t.N) break;
+        float4 a = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+        if (!p.first) {
+          const float4 o = *reinterpret_cast<const float4*>(accrow + col);
+          a.x += o.x;
+          a.y += o.y;
+          a.z += o.z;
+          a.w += o.w;
+        }
+        if (p.last_direct) {
+          uint2 h = make_uint2(pack_bf16x2(cs * a.x, cs * a.y), pack_bf16x2(cs * a.z, cs * a.w));
+          *reinterpret_cast<uint2*>(orow + col) = h;
+        } else {
+          *reinterpret_cast<float4*>(accrow + col) = a;
+        }
+      }
+    }
+  }
+};
+
+// ============================================================ S5 dW epilogue
+// acc = (G_c^T H)[vocab row, cols]; dW rows of the chunk = c * acc (or +=).
+struct EpiDW {
+  struct Params {
+    float* dW;            // chunk row 0 of dweight
+    int64_t ld;           // D
+    int32_t accumulate;
+    const Header* hdr;
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+    const float cs = p.hdr->c;
+    float* row = p.dW + static_cast<int64_t>(r) * p.ld;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      const int cb = t.n0 + c * 32;
+      if (!valid) continue;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int col = cb + 4 * v;
+        if (col >= t.N) break;
+        float4 a = make_float4(cs * x[4 * v], cs * x[4 * v + 1], cs * x[4 * v + 2], cs * x[4 * v + 3]);
+        if (p.accumulate) {
+          const float4 o = *reinterpret_cast<const float4*>(row + col);
+          a.x += o.x;
+          a.y += o.y;
+          a.z += o.z;
+          a.w += o.w;
+        }
+        *reinterpret_cast<float4*>(row + col) = a;
+      }
+    }
+  }
+};
+
+// ============================================================ diagnostics epilogue
+struct EpiStore {
+  struct Params {
+    float* C;
+    int64_t ldc;
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      if (!valid) continue;
+      for (int j = 0; j < 32; ++j) {
+        const int col = t.n0 + c * 32 + j;
+        if (col < t.N) p.C[static_cast<int64_t>(r) * p.ldc + col] = x[j];
+      }
+    }
+  }
+};
+
+// ============================================================ S0 prep
+// Label scan + stable compaction (one CTA, 1024 threads, 4 labels per thread
+// per pass).  Mask-first: only rows with y != ignore_index and y in
+// [0, V) enter idx[]; out-of-range labels set the status bit of this call.  Writes
+// N_v and the gradient scale c into the header, zeroes lse / token_loss of
+// excluded rows and zt of compacted rows.
+__global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ y, int N, int32_t ignore,
+                                                    int64_t vocab_total, int32_t* __restrict__ idx,
+                                                    int32_t* __restrict__ yc, float* __restrict__ zt,
+                                                    float* __restrict__ lse_out, float* __restrict__ tok_out,
+                                                    Header* hdr, const float* __restrict__ grad_loss,
+                                                    int reduction) {
+  __shared__ int warp_tot[32];
+  __shared__ int base_s;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) base_s = 0;
+  __syncthreads();
+  bool bad_any = false;
+  for (int start = 0; start < N; start += 4096) {
+    int flags[4];
+    int cnt = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = start + tid * 4 + u;
+      int f = 0;
+      if (i < N) {
+        const int32_t l = y[i];
+        if (l != ignore) {
+          if (l >= 0 && static_cast<int64_t>(l) < vocab_total) {
+            f = 1;
+          } else {
+            bad_any = true;
+          }
+        }
+        if (!f) {
+          if (lse_out) lse_out[i] = 0.f;
+          if (tok_out) tok_out[i] = 0.f;
+        }
+      }
+      flags[u] = f;
+      cnt += f;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int w = warp_tot[lane];
+      int wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += v;
+      }
+      warp_tot[lane] = wi - w;  // exclusive
+    }
+    __syncthreads();
+    int pos = base_s + warp_tot[wid] + incl - cnt;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (flags[u]) {
+        const int i = start + tid * 4 + u;
+        idx[pos] = i;
+        yc[pos] = y[i];
+        zt[pos] = 0.f;
+        ++pos;
+      }
+    }
+    __syncthreads();
+    if (tid == 1023) base_s = pos;
+    __syncthreads();
+  }
+  const int any_bad = __syncthreads_or(bad_any ? 1 : 0);
+  if (tid == 0) {
+    hdr->status = any_bad ? kStatusBadLabel : 0u;
+    const int nv = base_s;
+    hdr->n_valid = nv;
+    const float g = grad_loss ? *grad_loss : 1.f;
+    hdr->c = nv == 0 ? 0.f : (reduction == 0 ? g / static_cast<float>(nv) : g);
+    hdr->counter = 0u;
+  }
+}
+
+// ============================================================ S0 gather
+// Block b: compact row b <- H[idx[b]] (zeros for b in [N_v, ceil128(N_v)) so
+// whole 128-row tiles and 64-row k-blocks read finite zeros), optional lse
+// gather for the backward, optional zeroing of dhidden row b if token b is
+// excluded (ignored or bad label: its gradient is exactly 0).
+__global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict__ H, int64_t D, int N,
+                                                     const int32_t* __restrict__ idx, const Header* hdr,
+                                                     uint16_t* __restrict__ Hc, const float* __restrict__ lse_in,
+                                                     float* __restrict__ lse_c, const int32_t* __restrict__ y,
+                                                     int32_t ignore, int64_t vocab_total,
+                                                     uint16_t* __restrict__ dhidden) {
+  const int b = blockIdx.x;
+  const int nv = hdr->n_valid;
+  const int nvec = static_cast<int>(D / 8);
+  uint4* dst = reinterpret_cast<uint4*>(Hc + static_cast<int64_t>(b) * D);
+  if (b < nv) {
+    const int src_row = idx[b];
+    const uint4* src = reinterpret_cast<const uint4*>(H + static_cast<int64_t>(src_row) * D);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
+    if (lse_in && threadIdx.x == 0) lse_c[b] = lse_in[src_row];
+  } else if (b < ((nv + 127) & ~127)) {
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
+  }
+  if (dhidden && b < N) {
+    const int32_t l = y[b];
+    const bool kept = l != ignore && l >= 0 && static_cast<int64_t>(l) < vocab_total;
+    if (!kept) {
+      uint4* o = reinterpret_cast<uint4*>(dhidden + static_cast<int64_t>(b) * D);
+      for (int v = threadIdx.x; v < nvec; v += blockDim.x) o[v] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
+// ============================================================ S3 combine (+ loss)
+// mode 0 (one GPU): partials -> lse, token loss, loss (fixed-order, fp64 sum).
+// mode 1 (vocab-parallel, before the MAX all-reduce): partials -> local
+//   (m_loc, s_loc); m_loc also copied to m_glob for the in-place all-reduce.
+// mode 2 (after MAX all-reduce): s_loc *= exp(m_loc - M) for the SUM all-reduce.
+// mode 3 (after SUM all-reduce of (s, zt)): lse = M + ln s, token loss, loss.
+__device__ __forceinline__ void block_loss_reduce(double li, double* block_sums, Header* hdr, float* loss,
+                                                  int32_t* n_valid_out, int nv, int reduction) {
+  __shared__ double red[256];
+  __shared__ bool last;
+  red[threadIdx.x] = li;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    block_sums[blockIdx.x] = red[0];
+    __threadfence();
+    const uint32_t done = atomicAdd(&hdr->counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    // fixed-order final sum: each thread a strided slice, then the same tree
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += 256)
+      acc += reinterpret_cast<volatile double*>(block_sums)[i];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      double L = red[0];
+      if (reduction == 0) L = nv > 0 ? L / nv : 0.0;
+      if (hdr->status & kStatusBadLabel) L = __longlong_as_double(0x7ff8000000000000ULL);
+      *loss = static_cast<float>(L);
+      if (n_valid_out) *n_valid_out = nv;
+      hdr->counter = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) combine_kernel(int mode, const float* __restrict__ pm,
+                                                      const float* __restrict__ ps, int n_tiles, int64_t ld,
+                                                      float* __restrict__ m_loc, float* __restrict__ m_glob,
+                                                      float* __restrict__ s_buf, const float* __restrict__ zt,
+                                                      const int32_t* __restrict__ idx, Header* hdr,
+                                                      float* __restrict__ lse_out, float* __restrict__ tok_out,
+                                                      double* __restrict__ block_sums, float* __restrict__ loss,
+                                                      int32_t* __restrict__ n_valid_out, int reduction) {
+  const int r = blockIdx.x * 256 + threadIdx.x;
+  const int nv = hdr->n_valid;
+  const bool valid = r < nv;
+  if (mode == 0 || mode == 1) {
+    float M = -INFINITY, S = 0.f;
+    if (valid) {
+      for (int t = 0; t < n_tiles; ++t) M = fmaxf(M, pm[t * ld + r]);
+      for (int t = 0; t < n_tiles; ++t) S += ps[t * ld + r] * expf(pm[t * ld + r] - M);
+    }
+    if (mode == 1) {
+      if (valid) {
+        m_loc[r] = M;
+        m_glob[r] = M;
+        s_buf[r] = S;
+      }
+      return;
+    }
+    double li = 0.0;
+    if (valid) {
+      const float lse = M + logf(S);
+      const float l = lse - zt[r];
+      const int i = idx[r];
+      lse_out[i] = lse;
+      if (tok_out) tok_out[i] = l;
+      li = l;
+    }
+    block_loss_reduce(li, block_sums, hdr, loss, n_valid_out, nv, reduction);
+    return;
+  }
+  if (mode == 2) {
+    if (valid) s_buf[r] *= expf(m_loc[r] - m_glob[r]);
+    return;
+  }
+  // mode 3
+  double li = 0.0;
+  if (valid) {
+    const float lse = m_glob[r] + logf(s_buf[r]);
+    const float l = lse - zt[r];
+    const int i = idx[r];
+    lse_out[i] = lse;
+    if (tok_out) tok_out[i] = l;
+    li = l;
+  }
+  block_loss_reduce(li, block_sums, hdr, loss, n_valid_out, nv, reduction);
+}
+
+// ============================================================ S7 finalize (multi-GPU)
+// dhidden[idx[r]] = bf16(c * dH_sum[r]) after the cross-rank all-reduce.
+__global__ void __launch_bounds__(256) finalize_dh_kernel(const float* __restrict__ acc, int64_t D,
+                                                          const int32_t* __restrict__ idx, const Header* hdr,
+                                                          uint16_t* __restrict__ dhidden) {
+  const int r = blockIdx.x;
+  if (r >= hdr->n_valid) return;
+  const float c = hdr->c;
+  const float4* src = reinterpret_cast<const float4*>(acc + static_cast<int64_t>(r) * D);
+  uint2* dst = reinterpret_cast<uint2*>(dhidden + static_cast<int64_t>(idx[r]) * D);
+  for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
+    const float4 a = src[v];
+    dst[v] = make_uint2(pack_bf16x2(c * a.x, c * a.y), pack_bf16x2(c * a.z, c * a.w));
+  }
+}
+
+}  // namespace lce

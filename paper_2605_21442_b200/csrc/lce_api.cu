@@ -1,0 +1,606 @@
+// lce_api.cu -- C ABI of liblce.so (include/lce.h): argument validation,
+// workspace planning, TMA descriptor encoding, launch sequencing, the
+// vocab-parallel NCCL layer and the opt-in kernel profiler.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/lce.h"
+#include "kernels.cuh"
+#include "nccl.h"
+
+using namespace lce;
+
+namespace {
+
+// ------------------------------------------------------------------ helpers
+constexpr int64_t kDefaultChunkBudget = 512ll << 20;
+std::atomic<uint64_t> g_launches{0};
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+#define LCE_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: %s -> %s\n", #expr, cudaGetErrorString(e_)); \
+      return LCE_ERR_CUDA;                                                               \
+    }                                                                                    \
+  } while (0)
+
+// ------------------------------------------------------------------ workspace plan
+struct Plan {
+  int64_t N, D, Vl, cap, n_tiles, Vc, n_chunks, nblocks;
+  size_t hdr, idx, yc, zt, lsec, bsum, mloc, mglob, sbuf, hc, region, pm, ps, g, dh, total;
+};
+
+bool make_plan(const lce_problem_t* p, Plan* pl) {
+  if (!p) return false;
+  const int64_t N = p->n_tokens, D = p->hidden_dim, Vl = p->vocab_local;
+  if (N < 0 || D <= 0 || (D % 8) != 0 || Vl <= 0) return false;
+  if (p->vocab_start < 0 || p->vocab_total <= 0 || p->vocab_start + Vl > p->vocab_total) return false;
+  if (N >= (1ll << 31) - 256 || D >= (1ll << 31) || p->vocab_total >= (1ll << 31)) return false;
+  Plan q{};
+  q.N = N;
+  q.D = D;
+  q.Vl = Vl;
+  q.cap = round_up(N > 0 ? N : 1, BM);
+  q.n_tiles = ceil_div(Vl, BN);
+  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultChunkBudget;
+  int64_t vc = (budget / (q.cap * 2)) / BN * BN;
+  if (vc < BN) vc = BN;
+  if (vc > round_up(Vl, BN)) vc = round_up(Vl, BN);
+  q.Vc = vc;
+  q.n_chunks = ceil_div(Vl, vc);
+  q.nblocks = ceil_div(q.cap, 256);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = static_cast<size_t>(round_up(static_cast<int64_t>(off + bytes), 1024));
+    return o;
+  };
+  q.hdr = take(sizeof(Header));
+  q.idx = take(q.cap * 4);
+  q.yc = take(q.cap * 4);
+  q.zt = take(q.cap * 4);  // followed by sbuf? no: sbuf+zt must be adjacent for one all-reduce
+  q.lsec = take(q.cap * 4);
+  q.bsum = take(q.nblocks * 8);
+  q.mloc = take(q.cap * 4);
+  q.mglob = take(q.cap * 4);
+  q.sbuf = take(q.cap * 8);  // [s | zt_shadow]: s at sbuf, target logits copied after it
+  q.hc = take(static_cast<size_t>(q.cap * D * 2));
+  q.region = off;
+  const size_t fwd = static_cast<size_t>(2 * q.n_tiles * q.cap * 4) + 1024;
+  q.pm = q.region;
+  q.ps = q.region + static_cast<size_t>(round_up(q.n_tiles * q.cap * 4, 1024));
+  q.g = q.region;
+  q.dh = q.region + static_cast<size_t>(round_up(q.cap * q.Vc * 2, 1024));
+  const size_t bwd = (q.dh - q.region) + static_cast<size_t>(q.cap * D * 4);
+  q.total = q.region + (fwd > bwd ? fwd : bwd);
+  *pl = q;
+  return true;
+}
+
+// ------------------------------------------------------------------ device / driver
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+  });
+  return fn;
+}
+
+struct DevInfo {
+  bool ok;
+  int sms;
+};
+
+lce_status_t device_info(DevInfo* out) {
+  int dev = 0;
+  LCE_CUDA(cudaGetDevice(&dev));
+  static DevInfo cache[64];
+  static bool have[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && have[dev]) {
+    *out = cache[dev];
+    return out->ok ? LCE_OK : LCE_ERR_DEVICE;
+  }
+  int major = 0, minor = 0, sms = 0;
+  LCE_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  LCE_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+  LCE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DevInfo d{major == 10 && minor == 0, sms};
+  if (d.ok) {
+    // opt in to the dynamic shared memory every GEMM instantiation needs
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiLse>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, true, EpiDH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, true, EpiDW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, true, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, false, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, true, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+  }
+  if (dev < 64) {
+    cache[dev] = d;
+    have[dev] = true;
+  }
+  *out = d;
+  return d.ok ? LCE_OK : LCE_ERR_DEVICE;
+}
+
+// 2-D bf16 tensor map over a row-major [rows, inner] array with row pitch
+// `pitch` elements, box {64, box_rows}, 128-byte swizzle, zero OOB fill.
+lce_status_t encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int64_t pitch,
+                        int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return LCE_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch * 2)};
+  cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    if (getenv("LCE_DEBUG"))
+      fprintf(stderr, "lce: cuTensorMapEncodeTiled(%lld x %lld, pitch %lld, box %d) -> %d\n", (long long)inner,
+              (long long)rows, (long long)pitch, box_rows, (int)r);
+    return LCE_ERR_CUDA;
+  }
+  return LCE_OK;
+}
+
+// K-major operand stored [rows, K]: box {64 of K, box_rows}.
+lce_status_t map_kmajor(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t pitch, int box_rows) {
+  return encode_map(m, base, K, rows, pitch, box_rows);
+}
+// MN-major operand stored [K, MN]: boxes {64 of MN, BK rows of K}.
+lce_status_t map_mnmajor(CUtensorMap* m, const void* base, int64_t K, int64_t MN, int64_t pitch) {
+  return encode_map(m, base, MN, K, pitch, BK);
+}
+
+// ------------------------------------------------------------------ profiler
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+struct Profiler {
+  std::mutex mu;
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+} g_prof;
+
+struct LaunchScope {
+  int cls;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(int c, cudaStream_t st) : cls(c), s(st) {
+    if (g_prof.on) {
+      a = g_prof.get();
+      b = g_prof.get();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~LaunchScope() {
+    g_launches.fetch_add(cls == LCE_K_COMM ? 0 : 1);
+    if (a) {
+      cudaEventRecord(b, s);
+      g_prof.recs.push_back({cls, a, b});
+    }
+  }
+};
+
+inline lce_status_t last_error() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: launch error %s\n", cudaGetErrorString(e));
+    return LCE_ERR_CUDA;
+  }
+  return LCE_OK;
+}
+
+template <bool A_MN, bool B_MN, class Epi>
+lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d,
+                         const typename Epi::Params& ep, int sms, cudaStream_t s) {
+  LaunchScope sc(cls, s);
+  gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
+  return last_error();
+}
+
+// ------------------------------------------------------------------ NCCL (loaded at run time)
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*);
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*commDestroy)(ncclComm_t);
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*groupStart)();
+  ncclResult_t (*groupEnd)();
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return;
+    api.getUniqueId = reinterpret_cast<decltype(api.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<decltype(api.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.commDestroy = reinterpret_cast<decltype(api.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
+    api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
+  });
+  return api.ok ? &api : nullptr;
+}
+
+}  // namespace
+
+struct lce_comm_s {
+  ncclComm_t comm;
+  int nranks, rank;
+};
+
+namespace {
+
+lce_status_t allreduce(lce_comm_t c, void* buf, size_t count, ncclRedOp_t op, cudaStream_t s) {
+  NcclApi* api = nccl();
+  if (!api) return LCE_ERR_NCCL;
+  LaunchScope sc(LCE_K_COMM, s);
+  if (api->allReduce(buf, buf, count, ncclFloat32, op, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+  return LCE_OK;
+}
+
+lce_status_t validate(const lce_problem_t* p, lce_comm_t comm, size_t ws_bytes, const void* ws, Plan* pl) {
+  if (!p) return LCE_ERR_NULL;
+  if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM) return LCE_ERR_REDUCTION;
+  if (!make_plan(p, pl)) return LCE_ERR_SHAPE;
+  if (!ws) return LCE_ERR_NULL;
+  if (!aligned16(ws)) return LCE_ERR_ALIGN;
+  if (ws_bytes < pl->total) return LCE_ERR_WORKSPACE;
+  if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
+  return LCE_OK;
+}
+
+#define LCE_TRY(expr)                  \
+  do {                                 \
+    lce_status_t st_ = (expr);         \
+    if (st_ != LCE_OK) return st_;     \
+  } while (0)
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+int lce_abi_version(void) { return LCE_ABI_VERSION; }
+
+uint64_t lce_launch_count(void) { return g_launches.load(); }
+
+const char* lce_status_string(lce_status_t s) {
+  switch (s) {
+    case LCE_OK: return "ok";
+    case LCE_ERR_NULL: return "null pointer";
+    case LCE_ERR_SHAPE: return "invalid shape";
+    case LCE_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case LCE_ERR_REDUCTION: return "invalid reduction";
+    case LCE_ERR_WORKSPACE: return "workspace too small";
+    case LCE_ERR_LABEL_RANGE: return "label out of range";
+    case LCE_ERR_DEVICE: return "device is not sm_100 (B200)";
+    case LCE_ERR_CUDA: return "CUDA error";
+    case LCE_ERR_NCCL: return "NCCL error or NCCL unavailable";
+    case LCE_ERR_COMM: return "communicator does not match problem";
+  }
+  return "unknown status";
+}
+
+size_t lce_workspace_bytes(const lce_problem_t* p) {
+  Plan pl;
+  if (!make_plan(p, &pl)) return 0;
+  return pl.total;
+}
+
+lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+                         const int32_t* labels, float* loss, float* lse, float* token_loss, int32_t* n_valid,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  Plan pl;
+  LCE_TRY(validate(p, comm, workspace_bytes, workspace, &pl));
+  if (!weight || !loss) return LCE_ERR_NULL;
+  if (pl.N > 0 && (!hidden || !labels || !lse)) return LCE_ERR_NULL;
+  const void* ptrs[] = {hidden, weight, labels, loss, lse, token_loss, n_valid};
+  for (const void* q : ptrs)
+    if (q && !aligned16(q)) return LCE_ERR_ALIGN;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Header* hdr = reinterpret_cast<Header*>(ws + pl.hdr);
+
+  if (pl.N == 0) {  // empty batch: loss 0, N_v 0, nothing to project
+    LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
+    if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
+    return LCE_OK;
+  }
+  const int N = static_cast<int>(pl.N);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + pl.idx);
+  int32_t* yc = reinterpret_cast<int32_t*>(ws + pl.yc);
+  float* zt = reinterpret_cast<float*>(ws + pl.zt);
+  uint16_t* hc = reinterpret_cast<uint16_t*>(ws + pl.hc);
+  float* pm = reinterpret_cast<float*>(ws + pl.pm);
+  float* ps = reinterpret_cast<float*>(ws + pl.ps);
+  double* bsum = reinterpret_cast<double*>(ws + pl.bsum);
+  float* mloc = reinterpret_cast<float*>(ws + pl.mloc);
+  float* mglob = reinterpret_cast<float*>(ws + pl.mglob);
+  float* sbuf = reinterpret_cast<float*>(ws + pl.sbuf);
+
+  {  // S0: label scan + compaction
+    LaunchScope sc(LCE_K_PREP, s);
+    prep_kernel<<<1, 1024, 0, s>>>(labels, N, p->ignore_index, p->vocab_total, idx, yc, zt, lse, token_loss, hdr,
+                                   nullptr, p->reduction);
+    LCE_TRY(last_error());
+  }
+  {  // S0: gather valid rows of H
+    LaunchScope sc(LCE_K_GATHER, s);
+    gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, nullptr, nullptr,
+                                                               labels, p->ignore_index, p->vocab_total, nullptr);
+    LCE_TRY(last_error());
+  }
+  // S1+S2: logits tile by tile in TMEM, online LSE epilogue
+  CUtensorMap ta, tb;
+  LCE_TRY(map_kmajor(&ta, hc, pl.cap, pl.D, pl.D, BM));
+  LCE_TRY(map_kmajor(&tb, weight, pl.Vl, pl.D, pl.D, BN));
+  GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(pl.Vl)};
+  EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), static_cast<int32_t>(pl.Vl), pm, ps, pl.cap, zt};
+  LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s)));
+
+  const unsigned cblocks = static_cast<unsigned>(pl.nblocks);
+  const int nt = static_cast<int>(pl.n_tiles);
+  if (!comm) {  // S3 on one GPU: one fused combine + loss kernel
+    LaunchScope sc(LCE_K_COMBINE, s);
+    combine_kernel<<<cblocks, 256, 0, s>>>(0, pm, ps, nt, pl.cap, mloc, mglob, sbuf, zt, idx, hdr, lse, token_loss,
+                                           bsum, loss, n_valid, p->reduction);
+    return last_error();
+  }
+  {  // with a communicator (any size, including 1): local merge first
+    LaunchScope sc(LCE_K_COMBINE, s);
+    combine_kernel<<<cblocks, 256, 0, s>>>(1, pm, ps, nt, pl.cap, mloc, mglob, sbuf, zt, idx, hdr, lse, token_loss,
+                                           bsum, loss, n_valid, p->reduction);
+    LCE_TRY(last_error());
+  }
+  // vocab-parallel exchange: MAX of m, then SUM of (s * e^{m - M}, z_target)
+  float* sz = sbuf;                  // [cap] s followed by [cap] target logits
+  float* ztc = sbuf + pl.cap;
+  LCE_CUDA(cudaMemcpyAsync(ztc, zt, pl.cap * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  LCE_TRY(allreduce(comm, mglob, pl.cap, ncclMax, s));
+  {
+    LaunchScope sc(LCE_K_COMBINE, s);
+    combine_kernel<<<cblocks, 256, 0, s>>>(2, pm, ps, nt, pl.cap, mloc, mglob, sbuf, zt, idx, hdr, lse, token_loss,
+                                           bsum, loss, n_valid, p->reduction);
+    LCE_TRY(last_error());
+  }
+  LCE_TRY(allreduce(comm, sz, 2 * pl.cap, ncclSum, s));
+  {
+    LaunchScope sc(LCE_K_COMBINE, s);
+    combine_kernel<<<cblocks, 256, 0, s>>>(3, pm, ps, nt, pl.cap, mloc, mglob, sbuf, ztc, idx, hdr, lse,
+                                           token_loss, bsum, loss, n_valid, p->reduction);
+    LCE_TRY(last_error());
+  }
+  return LCE_OK;
+}
+
+lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+                          const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
+                          float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  Plan pl;
+  LCE_TRY(validate(p, comm, workspace_bytes, workspace, &pl));
+  if (!weight || !dweight) return LCE_ERR_NULL;
+  if (pl.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
+  const void* ptrs[] = {hidden, weight, labels, lse, grad_loss, dhidden, dweight};
+  for (const void* q : ptrs)
+    if (q && !aligned16(q)) return LCE_ERR_ALIGN;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Header* hdr = reinterpret_cast<Header*>(ws + pl.hdr);
+
+  if (pl.N == 0) {
+    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, pl.Vl * pl.D * sizeof(float), s));
+    return LCE_OK;
+  }
+  const int N = static_cast<int>(pl.N);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + pl.idx);
+  int32_t* yc = reinterpret_cast<int32_t*>(ws + pl.yc);
+  float* zt = reinterpret_cast<float*>(ws + pl.zt);
+  float* lsec = reinterpret_cast<float*>(ws + pl.lsec);
+  uint16_t* hc = reinterpret_cast<uint16_t*>(ws + pl.hc);
+  uint16_t* G = reinterpret_cast<uint16_t*>(ws + pl.g);
+  float* dh = reinterpret_cast<float*>(ws + pl.dh);
+  const bool multi = comm && comm->nranks >= 1;
+
+  {
+    LaunchScope sc(LCE_K_PREP, s);
+    prep_kernel<<<1, 1024, 0, s>>>(labels, N, p->ignore_index, p->vocab_total, idx, yc, zt, nullptr, nullptr, hdr,
+                                   grad_loss, p->reduction);
+    LCE_TRY(last_error());
+  }
+  {
+    LaunchScope sc(LCE_K_GATHER, s);
+    gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, lse, lsec, labels,
+                                                               p->ignore_index, p->vocab_total, dhidden);
+    LCE_TRY(last_error());
+  }
+  CUtensorMap t_hc_k, t_hc_mn, t_g_k, t_g_mn;
+  LCE_TRY(map_kmajor(&t_hc_k, hc, pl.cap, pl.D, pl.D, BM));
+  LCE_TRY(map_mnmajor(&t_hc_mn, hc, pl.cap, pl.D, pl.D));
+  LCE_TRY(map_kmajor(&t_g_k, G, pl.cap, pl.Vc, pl.Vc, BM));
+  LCE_TRY(map_mnmajor(&t_g_mn, G, pl.cap, pl.Vc, pl.Vc));
+
+  for (int64_t k = 0; k < pl.n_chunks; ++k) {
+    const int64_t v0 = k * pl.Vc;
+    const int64_t vc = (pl.Vl - v0) < pl.Vc ? (pl.Vl - v0) : pl.Vc;
+    const uint16_t* wc = weight + v0 * pl.D;
+    CUtensorMap t_w_k, t_w_mn;
+    LCE_TRY(map_kmajor(&t_w_k, wc, vc, pl.D, pl.D, BN));
+    LCE_TRY(map_mnmajor(&t_w_mn, wc, vc, pl.D, pl.D));
+    // S4: recompute logits of the chunk, G_c = softmax - onehot (bf16)
+    {
+      GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(vc)};
+      EpiG::Params ep{yc, lsec, static_cast<int32_t>(p->vocab_start + v0), static_cast<int32_t>(vc), G, pl.Vc};
+      LCE_TRY((launch_gemm<false, false, EpiG>(LCE_K_BWD_G, t_hc_k, t_w_k, d, ep, dev.sms, s)));
+    }
+    // S6: dH (+)= G_c W_c   (A = G_c K-major over vocab, B = W_c MN-major)
+    {
+      GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
+      EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx};
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
+    }
+    // S5: dW_c = c G_c^T H   (A = G_c MN-major, B = H_c MN-major, K = N_v)
+    {
+      GemmDims d{nullptr, static_cast<int32_t>(vc), &hdr->n_valid, 0, static_cast<int32_t>(pl.D)};
+      EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr};
+      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+    }
+  }
+  if (multi) {
+    // S7: dH summed over the vocab shards, then scaled, cast, scattered
+    LCE_TRY(allreduce(comm, dh, static_cast<size_t>(pl.N * pl.D), ncclSum, s));
+    LaunchScope sc(LCE_K_FINAL, s);
+    finalize_dh_kernel<<<static_cast<unsigned>(pl.N), 256, 0, s>>>(dh, pl.D, idx, hdr, dhidden);
+    LCE_TRY(last_error());
+  }
+  return LCE_OK;
+}
+
+lce_status_t lce_check_device_status(void* workspace, void* stream) {
+  if (!workspace) return LCE_ERR_NULL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Header h;
+  LCE_CUDA(cudaMemcpyAsync(&h, workspace, sizeof(Header), cudaMemcpyDeviceToHost, s));
+  LCE_CUDA(cudaStreamSynchronize(s));
+  if (h.status & kStatusBadLabel) return LCE_ERR_LABEL_RANGE;
+  return LCE_OK;
+}
+
+lce_status_t lce_comm_get_unique_id(uint8_t id[128]) {
+  if (!id) return LCE_ERR_NULL;
+  NcclApi* api = nccl();
+  if (!api) return LCE_ERR_NCCL;
+  ncclUniqueId u;
+  if (api->getUniqueId(&u) != ncclSuccess) return LCE_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(id, &u, 128);
+  return LCE_OK;
+}
+
+lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank) {
+  if (!comm || !id) return LCE_ERR_NULL;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return LCE_ERR_SHAPE;
+  NcclApi* api = nccl();
+  if (!api) return LCE_ERR_NCCL;
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  ncclComm_t c;
+  if (api->commInitRank(&c, nranks, u, rank) != ncclSuccess) return LCE_ERR_NCCL;
+  *comm = new lce_comm_s{c, nranks, rank};
+  return LCE_OK;
+}
+
+lce_status_t lce_comm_destroy(lce_comm_t comm) {
+  if (!comm) return LCE_OK;
+  NcclApi* api = nccl();
+  lce_status_t st = LCE_OK;
+  if (api && api->commDestroy(comm->comm) != ncclSuccess) st = LCE_ERR_NCCL;
+  delete comm;
+  return st;
+}
+
+int lce_comm_size(lce_comm_t comm) { return comm ? comm->nranks : 1; }
+int lce_comm_rank(lce_comm_t comm) { return comm ? comm->rank : 0; }
+
+lce_status_t lce_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  g_prof.on = on != 0;
+  return LCE_OK;
+}
+
+lce_status_t lce_profile_read(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT]) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  for (int i = 0; i < LCE_K_COUNT; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (launches) launches[i] = 0;
+  }
+  lce_status_t st = LCE_OK;
+  for (ProfRec& r : g_prof.recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+      st = LCE_ERR_CUDA;
+    if (ms) ms[r.cls] += t;
+    if (launches) launches[r.cls] += 1;
+    g_prof.pool.push_back(r.a);
+    g_prof.pool.push_back(r.b);
+  }
+  g_prof.recs.clear();
+  return st;
+}
+
+lce_status_t lce_debug_gemm(const uint16_t* A, const uint16_t* B, float* C, int64_t M, int64_t N, int64_t K,
+                            int a_mn, int b_mn, void* stream) {
+  if (!A || !B || !C) return LCE_ERR_NULL;
+  if (M <= 0 || N <= 0 || K <= 0 || M >= (1 << 30) || N >= (1 << 30) || K >= (1 << 30)) return LCE_ERR_SHAPE;
+  const int64_t lda = a_mn ? M : K, ldb = b_mn ? N : K;
+  if (lda % 8 || ldb % 8) return LCE_ERR_SHAPE;
+  if (!aligned16(A) || !aligned16(B) || !aligned16(C)) return LCE_ERR_ALIGN;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUtensorMap ta, tb;
+  if (a_mn) LCE_TRY(map_mnmajor(&ta, A, K, M, M));
+  else LCE_TRY(map_kmajor(&ta, A, M, K, K, BM));
+  if (b_mn) LCE_TRY(map_mnmajor(&tb, B, K, N, N));
+  else LCE_TRY(map_kmajor(&tb, B, N, K, K, BN));
+  GemmDims d{nullptr, static_cast<int32_t>(M), nullptr, static_cast<int32_t>(K), static_cast<int32_t>(N)};
+  EpiStore::Params ep{C, N};
+  if (!a_mn && !b_mn) return launch_gemm<false, false, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);
+  if (!a_mn && b_mn) return launch_gemm<false, true, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);
+  if (a_mn && !b_mn) return launch_gemm<true, false, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);
+  return launch_gemm<true, true, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);
+}
+
+}  // extern "C"

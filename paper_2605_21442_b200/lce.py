@@ -1,0 +1,224 @@
+"""PyTorch-facing binding of the C-ABI LCE library (argument marshalling only).
+
+PyTorch provides device memory, the current stream and the process group
+(for distributing the NCCL id); every step of the loss runs in liblce.so.
+Cites: PAPER.md P:166 (Sec. 4.2 LCE), P:132 (drop-in for CE), P:180 (loss
+parallel over the vocabulary).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from ._lib import KERNEL_CLASSES, LCE_K_COUNT, Problem, check, lib
+
+MEAN, SUM = 0, 1
+_RED = {"mean": MEAN, "sum": SUM}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_problem(n_tokens: int, hidden_dim: int, vocab_local: int, *, vocab_start: int = 0,
+                 vocab_total: Optional[int] = None, ignore_index: int = -100, reduction: str = "mean",
+                 chunk_budget_bytes: int = 0) -> Problem:
+    if reduction not in _RED:
+        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+    return Problem(n_tokens, hidden_dim, vocab_local, vocab_start,
+                   vocab_local if vocab_total is None else vocab_total, ignore_index, _RED[reduction],
+                   chunk_budget_bytes)
+
+
+def workspace_bytes(problem: Problem) -> int:
+    return int(lib.lce_workspace_bytes(ctypes.byref(problem)))
+
+
+class Workspace:
+    """Caller-owned device scratch, grown on demand and reused across calls."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf: Optional[torch.Tensor] = None
+
+    def get(self, nbytes: int, device) -> torch.Tensor:
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        return self.buf
+
+
+_default_ws: dict = {}
+
+
+def _ws_for(ws: Optional[Workspace], problem: Problem, device) -> torch.Tensor:
+    if ws is None:
+        ws = _default_ws.setdefault(str(device), Workspace())
+    need = workspace_bytes(problem)
+    if need == 0:
+        raise ValueError("invalid LCE problem shape")
+    return ws.get(need, device)
+
+
+def _check_inputs(hidden, weight, labels):
+    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise TypeError("hidden and weight must be bf16")
+    if labels.dtype != torch.int32:
+        raise TypeError("labels must be int32")
+    for t in (hidden, weight, labels):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("tensors must be contiguous CUDA tensors")
+
+
+class Comm:
+    """Vocab-parallel communicator (NCCL over NVLink) owned by the library."""
+
+    def __init__(self, handle: ctypes.c_void_p, world: int, rank: int):
+        self.handle = handle
+        self.world = world
+        self.rank = rank
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Comm":
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [None]
+        if rank == 0:
+            buf = ctypes.create_string_buffer(128)
+            check(lib.lce_comm_get_unique_id(buf), "lce_comm_get_unique_id")
+            obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        h = ctypes.c_void_p()
+        check(lib.lce_comm_init(ctypes.byref(h), obj[0], world, rank), "lce_comm_init")
+        return cls(h, world, rank)
+
+    @classmethod
+    def single(cls) -> "Comm":
+        """A one-rank communicator: exercises the exchange path on one GPU."""
+        buf = ctypes.create_string_buffer(128)
+        check(lib.lce_comm_get_unique_id(buf), "lce_comm_get_unique_id")
+        h = ctypes.c_void_p()
+        check(lib.lce_comm_init(ctypes.byref(h), bytes(buf.raw), 1, 0), "lce_comm_init")
+        return cls(h, 1, 0)
+
+    def close(self):
+        if self.handle:
+            check(lib.lce_comm_destroy(self.handle), "lce_comm_destroy")
+            self.handle = None
+
+
+def shard_range(vocab: int, world: int, rank: int):
+    """Contiguous vocab shard of `rank` (R19): V_l = ceil(V / P), last shorter."""
+    vl = -(-vocab // world)
+    start = min(vocab, rank * vl)
+    return start, min(vocab, start + vl) - start
+
+
+def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *, ignore_index: int = -100,
+            reduction: str = "mean", comm: Optional[Comm] = None, vocab_start: int = 0,
+            vocab_total: Optional[int] = None, with_token_loss: bool = False, workspace: Optional[Workspace] = None,
+            chunk_budget_bytes: int = 0, stream=None, out: Optional[dict] = None) -> dict:
+    """loss [1] fp32, lse [N] fp32 (0 on ignored rows), n_valid [1] int32, token_loss."""
+    _check_inputs(hidden, weight, labels)
+    N, D = hidden.shape
+    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
+    dev = hidden.device
+    ws = _ws_for(workspace, prob, dev)
+    if out is None:
+        out = {
+            "loss": torch.empty(1, dtype=torch.float32, device=dev),
+            "lse": torch.empty(N, dtype=torch.float32, device=dev),
+            "n_valid": torch.empty(1, dtype=torch.int32, device=dev),
+            "token_loss": torch.empty(N, dtype=torch.float32, device=dev) if with_token_loss else None,
+        }
+    check(lib.lce_forward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
+                          _ptr(labels), _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["token_loss"]),
+                          _ptr(out["n_valid"]), _ptr(ws), ws.numel(), _stream(stream)), "lce_forward")
+    return out
+
+
+def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, lse: torch.Tensor, *,
+             grad_loss: Optional[torch.Tensor] = None, ignore_index: int = -100, reduction: str = "mean",
+             comm: Optional[Comm] = None, vocab_start: int = 0, vocab_total: Optional[int] = None,
+             dhidden: Optional[torch.Tensor] = None, dweight: Optional[torch.Tensor] = None,
+             accumulate_dweight: bool = False, workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0,
+             stream=None):
+    """dhidden [N, D] bf16 and dweight [V_l, D] fp32 (overwritten or accumulated)."""
+    _check_inputs(hidden, weight, labels)
+    N, D = hidden.shape
+    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
+    dev = hidden.device
+    ws = _ws_for(workspace, prob, dev)
+    if dhidden is None:
+        dhidden = torch.empty_like(hidden)
+    if dweight is None:
+        dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
+    if grad_loss is not None:
+        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+    check(lib.lce_backward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
+                           _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(dweight),
+                           1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)), "lce_backward")
+    return dhidden, dweight
+
+
+def check_device_status(workspace: Optional[Workspace] = None, device=None, stream=None) -> None:
+    """Raises LceError(LCE_ERR_LABEL_RANGE) if a bad label was seen (syncs)."""
+    ws = workspace or _default_ws.get(str(device or torch.device("cuda", torch.cuda.current_device())))
+    if ws is None or ws.buf is None:
+        return
+    check(lib.lce_check_device_status(_ptr(ws.buf), _stream(stream)), "lce_check_device_status")
+
+
+class LinearCrossEntropyFunction(torch.autograd.Function):
+    """autograd wrapper: loss = CE(hidden @ weight^T, labels), mask-first, chunked."""
+
+    @staticmethod
+    def forward(ctx, hidden, weight, labels, ignore_index, reduction):
+        out = forward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)
+        ctx.save_for_backward(hidden, weight, labels, out["lse"])
+        ctx.cfg = (ignore_index, reduction)
+        return out["loss"].reshape(())
+
+    @staticmethod
+    def backward(ctx, g):
+        hidden, weight, labels, lse = ctx.saved_tensors
+        ignore_index, reduction = ctx.cfg
+        dh, dw = backward(hidden, weight, labels, lse, grad_loss=g.reshape(1), ignore_index=ignore_index,
+                          reduction=reduction)
+        return dh, dw.to(weight.dtype), None, None, None
+
+
+def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduction: str = "mean"):
+    return LinearCrossEntropyFunction.apply(hidden, weight, labels, ignore_index, reduction)
+
+
+def debug_gemm(A: torch.Tensor, B: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool) -> torch.Tensor:
+    """C = A B^T through the tcgen05 mainloop (diagnostics)."""
+    C = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    check(lib.lce_debug_gemm(_ptr(A), _ptr(B), _ptr(C), M, N, K, int(a_mn), int(b_mn), _stream()), "lce_debug_gemm")
+    return C
+
+
+def launch_count() -> int:
+    return int(lib.lce_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    check(lib.lce_profile_enable(1 if on else 0), "lce_profile_enable")
+
+
+def profile_read() -> dict:
+    ms = (ctypes.c_double * LCE_K_COUNT)()
+    n = (ctypes.c_int64 * LCE_K_COUNT)()
+    check(lib.lce_profile_read(ms, n), "lce_profile_read")
+    return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_CLASSES)}

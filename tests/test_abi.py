@@ -1,0 +1,140 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol the
+header declares, and its host-side validation/planning logic behaves as
+include/lce.h documents (no GPU needed: all these paths return before any
+CUDA call)."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "lce.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2605_21442_b200 import build
+
+    build.build()
+    from paper_2605_21442_b200 import _lib
+
+    return _lib
+
+
+def header_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lce_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_header_symbol(L):
+    names = header_functions()
+    assert len(names) >= 15
+    assert sorted(L.EXPORTS) == names
+    for n in names:
+        assert hasattr(L.lib, n), n
+
+
+def test_version_and_status_strings(L):
+    assert L.lib.lce_abi_version() == 1
+    for code in range(11):
+        s = L.lib.lce_status_string(code)
+        assert s and s != b"unknown status"
+    assert L.lib.lce_status_string(99) == b"unknown status"
+    assert L.lib.lce_launch_count() >= 0
+
+
+def prob(L, N=16384, D=4096, V=128256, **kw):
+    p = L.Problem(N, D, kw.get("vl", V), kw.get("vstart", 0), V, -100, kw.get("red", 0), kw.get("budget", 0))
+    return p
+
+
+def test_workspace_formula_bounded(L):
+    """H9 / P:166: the workspace is O(N D + N V/128 + budget), never the
+    N x V logits (bf16 N*V*2 bytes)."""
+    for (N, D, V) in [(8192, 2048, 128256), (16384, 4096, 128256), (16384, 3584, 152064), (65536, 8192, 128256)]:
+        w = L.lib.lce_workspace_bytes(ctypes.byref(prob(L, N, D, V)))
+        assert w > 0
+        assert w < N * V * 2, (N, D, V, w)
+    tiny = L.lib.lce_workspace_bytes(ctypes.byref(prob(L, 256, 64, 1000)))
+    assert 0 < tiny < 4 << 20
+    # budget only moves the G chunk: a smaller budget never needs more bytes
+    a = L.lib.lce_workspace_bytes(ctypes.byref(prob(L, budget=64 << 20)))
+    b = L.lib.lce_workspace_bytes(ctypes.byref(prob(L, budget=1 << 30)))
+    assert a < b
+
+
+@pytest.mark.parametrize("bad", [
+    dict(N=-1), dict(D=0), dict(D=12), dict(V=0), dict(vl=10, vstart=128250), dict(N=1 << 31),
+])
+def test_workspace_rejects_invalid_shapes(L, bad):
+    N = bad.get("N", 64)
+    D = bad.get("D", 64)
+    V = bad.get("V", 100)
+    p = L.Problem(N, D, bad.get("vl", V), bad.get("vstart", 0), V, -100, 0, 0)
+    assert L.lib.lce_workspace_bytes(ctypes.byref(p)) == 0
+
+
+def _fwd(L, p, ws_bytes=1 << 30, ws=0x10000, h=0x20000, w=0x30000, y=0x40000, loss=0x50000, lse=0x60000):
+    vp = ctypes.c_void_p
+    return L.lib.lce_forward(ctypes.byref(p) if p is not None else None, None, vp(h), vp(w), vp(y), vp(loss),
+                             vp(lse), None, None, vp(ws), ws_bytes, None)
+
+
+def test_host_validation_errors(L):
+    """Errors of include/lce.h that are detected before anything is enqueued."""
+    p = prob(L, 256, 64, 1000)
+    assert _fwd(L, None) == 1                       # LCE_ERR_NULL
+    bad_red = prob(L, 256, 64, 1000, red=7)
+    assert _fwd(L, bad_red) == 4                    # LCE_ERR_REDUCTION
+    assert _fwd(L, prob(L, 256, 60, 1000)) == 2     # D % 8 != 0 -> LCE_ERR_SHAPE
+    assert _fwd(L, p, ws_bytes=100) == 5            # LCE_ERR_WORKSPACE
+    assert _fwd(L, p, ws=0x10008) == 3              # misaligned workspace -> LCE_ERR_ALIGN
+    assert _fwd(L, p, h=0x20004) == 3               # misaligned hidden
+    assert _fwd(L, p, ws=0) == 1                    # NULL workspace
+    assert _fwd(L, p, w=0) == 1                     # NULL weight
+    shard = prob(L, 256, 64, 1000, vl=500, vstart=500)
+    assert _fwd(L, shard) == 10                     # shard without communicator -> LCE_ERR_COMM
+
+
+def test_backward_host_validation(L):
+    vp = ctypes.c_void_p
+    p = prob(L, 256, 64, 1000)
+    args = [vp(0x20000), vp(0x30000), vp(0x40000), vp(0x50000), None, vp(0x60000), vp(0x70000), 0, vp(0x10000),
+            1 << 30, None]
+    a2 = list(args)
+    a2[6] = None  # dweight NULL
+    assert L.lib.lce_backward(ctypes.byref(p), None, *a2) == 1
+    a3 = list(args)
+    a3[8] = vp(0x10001)
+    assert L.lib.lce_backward(ctypes.byref(p), None, *a3) == 3
+
+
+def test_comm_arguments(L):
+    h = ctypes.c_void_p()
+    assert L.lib.lce_comm_init(None, b"\0" * 128, 1, 0) == 1
+    assert L.lib.lce_comm_init(ctypes.byref(h), b"\0" * 128, 0, 0) == 2
+    assert L.lib.lce_comm_init(ctypes.byref(h), b"\0" * 128, 2, 2) == 2
+    assert L.lib.lce_comm_size(None) == 1 and L.lib.lce_comm_rank(None) == 0
+    assert L.lib.lce_comm_destroy(None) == 0
+
+
+def test_profiler_roundtrip_without_launches(L):
+    ms = (ctypes.c_double * L.LCE_K_COUNT)()
+    n = (ctypes.c_int64 * L.LCE_K_COUNT)()
+    assert L.lib.lce_profile_enable(1) == 0
+    assert L.lib.lce_profile_read(ms, n) == 0
+    assert list(n) == [0] * L.LCE_K_COUNT
+    assert L.lib.lce_profile_enable(0) == 0
+
+
+def test_product_path_has_no_oracle_or_fallback():
+    """The package never imports oracle/ and has no CPU fallback code path."""
+    pkg = os.path.join(ROOT, "paper_2605_21442_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert "oracle" not in src.replace("oracle/", "").replace("CPU oracle", ""), f
+            assert "torch.nn.functional.cross_entropy" not in src, f

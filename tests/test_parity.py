@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 CPU oracle.
+
+Bars (BASELINE.json north_star):
+  loss        |L_gpu - L_or| <= 2e-3 |L_or|
+  dH, dW      ||X_gpu - X_or||_F <= 1e-2 ||X_or||_F
+  lse         |lse_gpu - lse_or| <= 1e-3 max(1, |lse_or|)
+  ignored rows: lse = token loss = dH row = 0 exactly.
+The oracle always consumes the exact bf16 values the GPU consumed.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import lce_backward, lce_forward, lce_rows
+from synth.inputs import CONFIGS, IGNORE, make_config, make_inputs, packed_labels
+
+pytestmark = pytest.mark.gpu
+
+LOSS_TOL, GRAD_TOL, LSE_TOL = 2e-3, 1e-2, 1e-3
+
+
+def gpu_run(inp, reduction="mean", grad=None, budget=0, comm=None, accumulate_into=None):
+    import paper_2605_21442_b200 as F
+
+    out = F.forward(inp.hidden, inp.weight, inp.labels, ignore_index=inp.ignore_index, reduction=reduction,
+                    with_token_loss=True, chunk_budget_bytes=budget, comm=comm)
+    g = None if grad is None else torch.tensor([grad], dtype=torch.float32, device=inp.hidden.device)
+    dw0 = None if accumulate_into is None else accumulate_into.clone()
+    dh, dw = F.backward(inp.hidden, inp.weight, inp.labels, out["lse"], grad_loss=g, ignore_index=inp.ignore_index,
+                        reduction=reduction, chunk_budget_bytes=budget, comm=comm, dweight=dw0,
+                        accumulate_dweight=accumulate_into is not None)
+    torch.cuda.synchronize()
+    return {
+        "loss": out["loss"].item(),
+        "n_valid": int(out["n_valid"].item()),
+        "lse": out["lse"].cpu().double().numpy(),
+        "tok": out["token_loss"].cpu().double().numpy(),
+        "dH": dh.float().cpu().double().numpy(),
+        "dW": dw.cpu().double().numpy(),
+    }
+
+
+def np_inputs(inp):
+    return (inp.hidden.float().cpu().numpy(), inp.weight.float().cpu().numpy(), inp.labels.cpu().numpy())
+
+
+def oracle_run(inp, reduction="mean", grad=1.0):
+    H, W, y = np_inputs(inp)
+    f = lce_forward(H, W, y, ignore_index=inp.ignore_index, reduction=reduction)
+    b = lce_backward(H, W, y, ignore_index=inp.ignore_index, reduction=reduction, grad_loss=grad)
+    return {"loss": f["loss"], "n_valid": f["n_valid"], "lse": f["lse"], "tok": f["token_loss"], "dH": b["dH"],
+            "dW": b["dW"]}
+
+
+def fro_rel(a, b):
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return float(np.linalg.norm(a))
+    return float(np.linalg.norm(a - b) / nb)
+
+
+def assert_parity(g, o, labels, ignore=IGNORE):
+    assert g["n_valid"] == o["n_valid"]
+    if o["loss"] == 0:
+        assert g["loss"] == 0
+    else:
+        assert abs(g["loss"] - o["loss"]) <= LOSS_TOL * abs(o["loss"]), (g["loss"], o["loss"])
+    lerr = np.abs(g["lse"] - o["lse"]) / np.maximum(1.0, np.abs(o["lse"]))
+    assert lerr.max() <= LSE_TOL, lerr.max()
+    terr = np.abs(g["tok"] - o["tok"]) / np.maximum(1.0, np.abs(o["lse"]))
+    assert terr.max() <= LSE_TOL, terr.max()
+    assert fro_rel(g["dH"], o["dH"]) <= GRAD_TOL, fro_rel(g["dH"], o["dH"])
+    assert fro_rel(g["dW"], o["dW"]) <= GRAD_TOL, fro_rel(g["dW"], o["dW"])
+    ign = labels == ignore
+    assert np.all(g["lse"][ign] == 0) and np.all(g["tok"][ign] == 0)
+    assert np.all(g["dH"][ign] == 0)
+
+
+# ------------------------------------------------------------ mainloop descriptors
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (64, 40, 16), (136, 264, 72)])
+def test_debug_gemm_matches_fp64(cuda_lib, a_mn, b_mn, M, N, K):
+    """The tcgen05 mainloop (smem/instruction descriptors, TMA swizzle, both
+    operand majors, ragged M/N/K tails) computes A B^T."""
+    import paper_2605_21442_b200 as F
+
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + 10 * a_mn + b_mn)
+    A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
+    As = A.t().contiguous() if a_mn else A
+    Bs = B.t().contiguous() if b_mn else B
+    C = F.debug_gemm(As, Bs, M, N, K, bool(a_mn), bool(b_mn))
+    torch.cuda.synchronize()
+    ref = A.double().cpu() @ B.double().cpu().T
+    err = (C.double().cpu() - ref).abs().max().item()
+    assert err <= 1e-4 * math.sqrt(K) * max(1.0, ref.abs().max().item()), err
+
+
+# ------------------------------------------------------------ tiny config (full oracle)
+@pytest.mark.parametrize("reduction", ["mean", "sum"])
+@pytest.mark.parametrize("regime", ["random", "confident"])
+def test_tiny_config(cuda_lib, reduction, regime):
+    inp = make_config("tiny", device="cuda", regime=regime)
+    g = gpu_run(inp, reduction)
+    o = oracle_run(inp, reduction)
+    assert_parity(g, o, inp.labels.cpu().numpy())
+
+
+# ------------------------------------------------------------ exact (D, V) of every config, reduced N
+@pytest.mark.parametrize("name", ["llama1b", "llama8b", "qwen7b", "llama70b"])
+def test_config_shapes_reduced_n(cuda_lib, name):
+    """Each BASELINE config's exact (D, V) (incl. the vocab tail tile) with a
+    ragged N spanning several 128-row tiles; 10% ignored rows (qwen: the packed
+    label structure)."""
+    c = CONFIGS[name]
+    N = 300
+    labels = None
+    if c["labels"] == "packed":
+        labels = packed_labels(2048, c["V"], seed=0)[:N]
+    inp = make_inputs(N, c["D"], c["V"], k=c["k"], device="cuda", ignore_frac=0.1, label_override=labels,
+                      regime="confident" if name == "llama8b" else "random")
+    g = gpu_run(inp, "mean")
+    o = oracle_run(inp, "mean")
+    assert_parity(g, o, inp.labels.cpu().numpy())
+
+
+# ------------------------------------------------------------ edge cases
+def small(N, D, V, seed=0, ignore_frac=0.1, labels=None, regime="random"):
+    return make_inputs(N, D, V, k=seed, device="cuda", ignore_frac=ignore_frac, label_override=labels, regime=regime)
+
+
+@pytest.mark.parametrize("N,D,V", [(1, 64, 1000), (127, 64, 257), (129, 72, 256), (200, 8, 513), (260, 136, 2)])
+def test_ragged_shapes(cuda_lib, N, D, V):
+    inp = small(N, D, V, seed=N)
+    assert_parity(gpu_run(inp), oracle_run(inp), inp.labels.cpu().numpy())
+
+
+def test_single_class_vocab(cuda_lib):
+    """V = 1: softmax is 1, loss 0, every gradient 0."""
+    inp = small(100, 64, 1, labels=np.zeros(100, dtype=np.int32))
+    g = gpu_run(inp)
+    assert g["n_valid"] == 100 and abs(g["loss"]) <= 1e-6
+    assert np.abs(g["dH"]).max() <= 1e-6 and np.abs(g["dW"]).max() <= 1e-6
+
+
+def test_empty_and_all_ignored(cuda_lib):
+    """N = 0 and N_v = 0: loss 0, lse 0, dH 0, dW 0."""
+    inp = small(0, 64, 1000)
+    g = gpu_run(inp)
+    assert g["loss"] == 0 and g["n_valid"] == 0 and not g["dW"].any()
+    lab = np.full(300, IGNORE, dtype=np.int32)
+    inp = small(300, 64, 1000, labels=lab)
+    for red in ("mean", "sum"):
+        g = gpu_run(inp, red)
+        assert g["loss"] == 0 and g["n_valid"] == 0
+        assert not g["lse"].any() and not g["dH"].any() and not g["dW"].any()
+
+
+def test_label_edges_and_ignore_inside_range(cuda_lib):
+    """Labels at 0, V-1 and both sides of the 256-column tile boundaries; an
+    ignore_index that is a legal vocab id (R3)."""
+    V = 1000
+    lab = np.array([0, V - 1, 255, 256, 511, 512, 767, 768, 5, 5] * 20, dtype=np.int32)
+    inp = small(len(lab), 64, V, labels=lab)
+    assert_parity(gpu_run(inp), oracle_run(inp), lab)
+    inp.ignore_index = 5
+    g = gpu_run(inp)
+    o = oracle_run(inp)
+    assert_parity(g, o, lab, ignore=5)
+
+
+def test_bad_label_poisons_loss_and_sets_status(cuda_lib):
+    """R4: a label outside [0, V) excludes its row, makes the loss NaN and is
+    reported by lce_check_device_status."""
+    import paper_2605_21442_b200 as F
+
+    lab = np.arange(200, dtype=np.int32) % 1000
+    lab[17] = 1000
+    inp = small(200, 64, 1000, labels=lab)
+    out = F.forward(inp.hidden, inp.weight, inp.labels, with_token_loss=True)
+    torch.cuda.synchronize()
+    assert math.isnan(out["loss"].item())
+    assert out["n_valid"].item() == 199
+    assert out["lse"][17].item() == 0
+    with pytest.raises(F.LceError) as e:
+        F.check_device_status(device=inp.hidden.device)
+    assert e.value.code == 6
+    lab[17] = 3
+    ok = small(200, 64, 1000, labels=lab)
+    F.forward(ok.hidden, ok.weight, ok.labels)
+    F.check_device_status(device=inp.hidden.device)  # status reflects the latest call
+
+
+def test_grad_scale_sum_and_accumulate(cuda_lib):
+    """R11: upstream gradient scales dH/dW; accumulate_dweight adds into dW."""
+    inp = small(300, 64, 1000, seed=3)
+    o = oracle_run(inp, "sum", grad=-2.5)
+    g = gpu_run(inp, "sum", grad=-2.5)
+    assert_parity(g, o, inp.labels.cpu().numpy())
+    base = torch.randn(1000, 64, device="cuda")
+    ga = gpu_run(inp, "sum", grad=-2.5, accumulate_into=base)
+    assert fro_rel(ga["dW"] - base.cpu().double().numpy(), o["dW"]) <= GRAD_TOL
+
+
+def test_chunk_budget_is_not_semantics(cuda_lib):
+    """R7: several vocab chunks (tiny budget) give the same result as one."""
+    inp = small(384, 128, 3000, seed=4)
+    one = gpu_run(inp)
+    many = gpu_run(inp, budget=384 * 2 * 256)  # one 256-column tile per chunk
+    o = oracle_run(inp)
+    assert_parity(many, o, inp.labels.cpu().numpy())
+    assert many["loss"] == one["loss"]
+    np.testing.assert_array_equal(many["lse"], one["lse"])
+    np.testing.assert_array_equal(many["dW"], one["dW"])
+    assert fro_rel(many["dH"], one["dH"]) <= 1e-2
+
+
+def test_garbage_in_ignored_rows_is_bitwise_invisible(cuda_lib):
+    """P3 mask-first: NaN/Inf in ignored rows of H never reaches the
+    projection: every output is bitwise unchanged and their dH rows are 0."""
+    inp = small(300, 128, 1000, seed=5, ignore_frac=0.3)
+    g0 = gpu_run(inp)
+    ign = inp.labels == IGNORE
+    h = inp.hidden.clone()
+    h[ign] = float("nan")
+    h[torch.nonzero(ign)[0, 0]] = float("inf")
+    inp.hidden = h
+    g1 = gpu_run(inp)
+    for k in ("lse", "tok", "dH", "dW"):
+        np.testing.assert_array_equal(g0[k], g1[k])
+    assert g0["loss"] == g1["loss"]
+
+
+def test_deterministic_rerun(cuda_lib):
+    """H8: fixed-order reductions and single-writer tiles -> bitwise reruns."""
+    inp = small(500, 256, 5000, seed=6)
+    a, b = gpu_run(inp), gpu_run(inp)
+    for k in ("lse", "tok", "dH", "dW"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert a["loss"] == b["loss"]
+
+
+def test_single_rank_communicator_path(cuda_lib):
+    """The vocab-parallel exchange (MAX / SUM all-reduce + finalize) on a
+    one-rank NCCL communicator matches the oracle."""
+    import paper_2605_21442_b200 as F
+
+    comm = F.Comm.single()
+    try:
+        inp = small(300, 64, 1000, seed=7)
+        g = gpu_run(inp, comm=comm)
+        assert_parity(g, oracle_run(inp), inp.labels.cpu().numpy())
+    finally:
+        comm.close()
+
+
+def test_autograd_function(cuda_lib):
+    import paper_2605_21442_b200 as F
+
+    inp = small(200, 64, 1000, seed=8)
+    h = inp.hidden.clone().requires_grad_(True)
+    w = inp.weight.clone().requires_grad_(True)
+    loss = F.linear_cross_entropy(h, w, inp.labels)
+    loss.backward()
+    o = oracle_run(inp)
+    assert abs(loss.item() - o["loss"]) <= LOSS_TOL * abs(o["loss"])
+    assert fro_rel(h.grad.float().cpu().double().numpy(), o["dH"]) <= GRAD_TOL
+    assert fro_rel(w.grad.float().cpu().double().numpy(), o["dW"]) <= 2e-2  # dW rounded to bf16 for autograd
+
+
+# ------------------------------------------------------------ full size, bench launch configuration
+@pytest.mark.parametrize("name", ["llama8b", "qwen7b"])
+def test_full_size_sampled_rows_and_invariants(cuda_lib, name):
+    """At the bench's full size: sampled rows (lse, token loss, dH) vs the
+    oracle row by row; loss == mean of token losses; sum_j dW_j ~ 0 (P2)."""
+    inp = make_config(name, device="cuda")
+    g = gpu_run(inp)
+    H, W, y = np_inputs(inp)
+    rng = np.random.default_rng(0)
+    rows = np.sort(rng.choice(len(y), size=48, replace=False))
+    rows = np.concatenate([rows, [0, len(y) - 1]])
+    o = lce_rows(H, W, y, rows, n_valid=g["n_valid"])
+    lerr = np.abs(g["lse"][rows] - o["lse"]) / np.maximum(1, np.abs(o["lse"]))
+    assert lerr.max() <= LSE_TOL
+    assert np.abs(g["tok"][rows] - o["token_loss"]).max() <= LSE_TOL * np.abs(o["lse"]).max()
+    assert fro_rel(g["dH"][rows], o["dH"]) <= GRAD_TOL
+    nv = int((y != IGNORE).sum())
+    assert g["n_valid"] == nv
+    assert abs(g["loss"] - g["tok"].sum() / nv) <= 1e-4 * abs(g["loss"])
+    col = np.linalg.norm(g["dW"].sum(axis=0))
+    assert col <= 1e-2 * np.linalg.norm(g["dW"]) * math.sqrt(1.0)
