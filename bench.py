@@ -118,17 +118,13 @@ def cpu_threads():
 
 def time_oracle(cfg_name: str, target_s: float = 12.0):
     """Oracle fwd+bwd on a bounded row sample; returns (tokens/s, rows, seconds)."""
-    H, W, y = oracle_sample(cfg_name, 4)
+    # calibrate on 128 rows (all oracle costs are linear in the row count), then
+    # size the sample for ~target_s seconds of fp64 work
+    H, W, y = oracle_sample(cfg_name, 128)
     t0 = time.perf_counter()
     run_oracle_step(H, W, y)
-    t_small = time.perf_counter() - t0
-    # the dW GEMM (V x D output) has a fixed cost; scale rows on the per-row slope
-    H2, W2, y2 = oracle_sample(cfg_name, 16)
-    t0 = time.perf_counter()
-    run_oracle_step(H2, W2, y2)
-    t16 = time.perf_counter() - t0
-    per_row = max((t16 - t_small) / 12, 1e-4)
-    n = int(max(8, min(CONFIGS[cfg_name]["N"], (target_s - t_small) / per_row)))
+    t128 = time.perf_counter() - t0
+    n = int(max(16, min(CONFIGS[cfg_name]["N"], 128 * target_s / max(t128, 1e-3))))
     H3, W3, y3 = oracle_sample(cfg_name, n)
     t0 = time.perf_counter()
     nv = run_oracle_step(H3, W3, y3)
@@ -140,9 +136,15 @@ def reference_arm(args, rank):
     if rank != 0:
         return
     c = CONFIGS[args.config]
-    _, n, nv, dt = time_oracle(args.config, target_s=8.0)
+    # each step is a bounded row sample sized so the whole run stays ~1-2 minutes
+    target = min(8.0, max(1.0, 60.0 / max(1, args.steps + min(args.warmup, 1))))
+    H, W, y = oracle_sample(args.config, 128)
+    t0 = time.perf_counter()
+    run_oracle_step(H, W, y)
+    t128 = time.perf_counter() - t0
+    n = int(max(16, min(c["N"], 128 * target / max(t128, 1e-3))))
     H, W, y = oracle_sample(args.config, n)
-    for _ in range(args.warmup if args.warmup < 1 else 1):
+    for _ in range(min(args.warmup, 1)):
         run_oracle_step(H, W, y)
     times = []
     for _ in range(args.steps):
@@ -223,7 +225,7 @@ def main():
                    workspace=ws)
 
     torch.cuda.reset_peak_memory_stats(dev)
-    for _ in range(max(args.warmup, 3 if args.warmup >= 3 else args.warmup)):
+    for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if dist:

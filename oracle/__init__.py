@@ -13,5 +13,6 @@ from .lce_oracle import (  # noqa: F401
     lce_backward,
     lce_rows,
     shard_stats,
+    shard_backward,
     combine_shard_stats,
 )

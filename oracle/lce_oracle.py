@@ -45,6 +45,7 @@ __all__ = [
     "lce_backward",
     "lce_rows",
     "shard_stats",
+    "shard_backward",
     "combine_shard_stats",
 ]
 
@@ -208,6 +209,32 @@ def shard_stats(hidden, weight_shard, labels, vocab_start: int, vocab_total: int
         own = (local >= 0) & (local < Wr.shape[0])
         zt[rows[own]] = z[np.flatnonzero(own), local[own]]
     return {"m": m, "s": s, "z_target": zt, "valid": valid}
+
+
+def shard_backward(hidden, weight_shard, labels, vocab_start: int, lse, c: float,
+                   ignore_index: int = IGNORE_INDEX) -> dict:
+    """Gradient contributions of one vocab shard given the global lse.
+
+    With G_r the shard's columns of G = c (softmax - onehot):
+    dH = sum_r G_r W_r (summed across shards) and dW rows of the shard = G_r^T H.
+    """
+    H = _as_f64(hidden)
+    Wr = _as_f64(weight_shard)
+    y = np.asarray(labels, dtype=np.int64)
+    lse = np.asarray(lse, dtype=np.float64)
+    rows = np.flatnonzero(y != ignore_index)
+    dH = np.zeros_like(H)
+    dW = np.zeros_like(Wr)
+    if rows.size:
+        z = H[rows] @ Wr.T
+        G = np.exp(z - lse[rows][:, None])
+        local = y[rows] - vocab_start
+        own = np.flatnonzero((local >= 0) & (local < Wr.shape[0]))
+        G[own, local[own]] -= 1.0
+        G *= c
+        dH[rows] = G @ Wr
+        dW = G.T @ H[rows]
+    return {"dH_partial": dH, "dW_shard": dW}
 
 
 def combine_shard_stats(stats: list) -> dict:

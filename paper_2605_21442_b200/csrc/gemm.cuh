@@ -213,6 +213,178 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
+// =====================================================================
+// CTA-pair variant: tcgen05.mma.cta_group::2, tile 256 x 256 per pair.
+//
+// A cluster of 2 CTAs on one TPC computes a 256-row x 256-col tile.  CTA r
+// stages rows [128r, 128r+128) of the A tile and columns [128r, 128r+128) of
+// the B tile (TMA .cta_group::2; both CTAs' bytes complete on the leader's
+// barrier); the leader's single MMA thread issues 256x256x16 MMAs that read
+// A and B from both CTAs' shared memory and write rows [128r, +128) of the
+// accumulator into CTA r's TMEM.  Per SM this halves the B operand's smem and
+// L2 traffic relative to the single-CTA kernel for the same MMA rate.
+// Epilogues are unchanged: each CTA drains its own 128 TMEM lanes.
+// =====================================================================
+constexpr int kPairBM = 256;  // rows per pair tile
+constexpr int kPairStages = 6;
+constexpr int kPairStageBytes = 128 * BK * 2 * 2;  // A half + B half = 32 KB
+constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 1024 + 256;
+
+template <bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmDims dims, const typename Epi::Params ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int kHalf = 128 * BK * 2;  // 16 KB
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kPairStages * kHalf;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kPairStages * kHalf);
+  uint64_t* empty = full + kPairStages;
+  uint64_t* tfull = empty + kPairStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  const int M = dev_or(dims.m_dev, dims.m_static);
+  const int K = dev_or(dims.k_dev, dims.k_static);
+  const int N = dims.n;
+  const int num_m = (M + kPairBM - 1) / kPairBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_k = (K + BK - 1) / BK;
+  const int num_tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kPairStages; ++s) {
+      mbar_init(&full[s], 1);   // leader: its own arrive.expect_tx; bytes from both CTAs
+      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);   // multicast commit
+      mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, kTmemCols);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && num_k > 0) {
+      // ---------------------------------------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        int mb, nb;
+        tile_of(t, num_m, num_n, mb, nb);
+        const int ma = mb * kPairBM + 128 * rank;  // this CTA's A rows
+        const int nbh = nb * BN + 128 * rank;      // this CTA's B rows (N half)
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+          uint8_t* a = sA + stage * kHalf;
+          uint8_t* b = sB + stage * kHalf;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_pair(a, &tmA, &full[stage], k0, ma);
+          } else {
+            tma_load_2d_pair(a, &tmA, &full[stage], ma, k0);
+            tma_load_2d_pair(a + BK * 128, &tmA, &full[stage], ma + 64, k0);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(b, &tmB, &full[stage], k0, nbh);
+          } else {
+            tma_load_2d_pair(b, &tmB, &full[stage], nbh, k0);
+            tma_load_2d_pair(b + BK * 128, &tmB, &full[stage], nbh + 64, k0);
+          }
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------------------------------------------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16_f32(kPairBM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * kHalf);
+          const uint32_t b_addr = smem_u32(sB + stage * kHalf);
+#pragma unroll
+          for (int kk = 0; kk < BK / UK; ++kk) {
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + kk * (UK * 128), BK * 128, 1024)
+                                     : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
+                                     : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
+            mma_bf16_ss_pair(d, ad, bd, idesc, (kb | kk) != 0);
+          }
+          mma_commit_pair(&empty[stage], 0x3);  // frees this stage in both CTAs
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (num_k > 0) {
+          mma_commit_pair(&tfull[acc], 0x3);
+        } else {
+          mbar_arrive_cluster(&tfull[acc], 0);
+          mbar_arrive_cluster(&tfull[acc], 1);
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      int mb, nb;
+      tile_of(t, num_m, num_n, mb, nb);
+      mbar_wait_cluster(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+      TileInfo ti{mb * kPairBM + 128 * static_cast<int>(rank), nb * BN, nb, M, N, q * 32 + lane, num_k == 0};
+      Epi::apply(ep, taddr, ti);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+}
+
 // Loads the 32-column chunk `c` of this thread's accumulator row as floats.
 __device__ __forceinline__ void load_chunk(uint32_t taddr, int c, bool zero, float (&x)[32]) {
   uint32_t v[32];

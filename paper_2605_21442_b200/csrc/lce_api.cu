@@ -53,7 +53,7 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.N = N;
   q.D = D;
   q.Vl = Vl;
-  q.cap = round_up(N > 0 ? N : 1, BM);
+  q.cap = round_up(N > 0 ? N : 1, kPairBM);  // whole 256-row pair tiles (G rows are written per tile)
   q.n_tiles = ceil_div(Vl, BN);
   const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultChunkBudget;
   int64_t vc = (budget / (q.cap * 2)) / BN * BN;
@@ -71,12 +71,12 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.hdr = take(sizeof(Header));
   q.idx = take(q.cap * 4);
   q.yc = take(q.cap * 4);
-  q.zt = take(q.cap * 4);  // followed by sbuf? no: sbuf+zt must be adjacent for one all-reduce
+  q.zt = take(q.cap * 4);
   q.lsec = take(q.cap * 4);
   q.bsum = take(q.nblocks * 8);
   q.mloc = take(q.cap * 4);
   q.mglob = take(q.cap * 4);
-  q.sbuf = take(q.cap * 8);  // [s | zt_shadow]: s at sbuf, target logits copied after it
+  q.sbuf = take(q.cap * 8);  // [s | z_t copy]: one SUM all-reduce of both
   q.hc = take(static_cast<size_t>(q.cap * D * 2));
   q.region = off;
   const size_t fwd = static_cast<size_t>(2 * q.n_tiles * q.cap * 4) + 1024;
@@ -131,14 +131,18 @@ lce_status_t device_info(DevInfo* out) {
   DevInfo d{major == 10 && minor == 0, sms};
   if (d.ok) {
     // opt in to the dynamic shared memory every GEMM instantiation needs
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiLse>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, true, EpiDH>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, true, EpiDW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, false, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<false, true, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, false, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
-    LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<true, true, EpiStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+#define LCE_SMEM_ATTR(A, B, E)                                                                                 \
+  LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)); \
+  LCE_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemBytes))
+    LCE_SMEM_ATTR(false, false, EpiLse);
+    LCE_SMEM_ATTR(false, false, EpiG);
+    LCE_SMEM_ATTR(false, true, EpiDH);
+    LCE_SMEM_ATTR(true, true, EpiDW);
+    LCE_SMEM_ATTR(false, false, EpiStore);
+    LCE_SMEM_ATTR(false, true, EpiStore);
+    LCE_SMEM_ATTR(true, false, EpiStore);
+    LCE_SMEM_ATTR(true, true, EpiStore);
+#undef LCE_SMEM_ATTR
   }
   if (dev < 64) {
     cache[dev] = d;
@@ -230,11 +234,41 @@ inline lce_status_t last_error() {
   return LCE_OK;
 }
 
+// GEMM variant: CTA pairs (tcgen05 cta_group::2, 256x256 tiles) by default;
+// LCE_GEMM=single selects the one-CTA 128x256 mainloop (A/B comparisons).
+bool use_pair() {
+  const char* e = getenv("LCE_GEMM");
+  return !(e && strcmp(e, "single") == 0);
+}
+// Rows of the TMA box of a K-major B operand: each CTA of a pair stages half of
+// the 256-column tile.
+int b_box_rows() { return use_pair() ? BN / 2 : BN; }
+
 template <bool A_MN, bool B_MN, class Epi>
 lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d,
                          const typename Epi::Params& ep, int sms, cudaStream_t s) {
   LaunchScope sc(cls, s);
-  gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
+  if (!use_pair()) {
+    gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
+    return last_error();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kPairSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
+  if (e != cudaSuccess) {
+    if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: cudaLaunchKernelEx -> %s\n", cudaGetErrorString(e));
+    return LCE_ERR_CUDA;
+  }
   return last_error();
 }
 
@@ -383,7 +417,7 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
   // S1+S2: logits tile by tile in TMEM, online LSE epilogue
   CUtensorMap ta, tb;
   LCE_TRY(map_kmajor(&ta, hc, pl.cap, pl.D, pl.D, BM));
-  LCE_TRY(map_kmajor(&tb, weight, pl.Vl, pl.D, pl.D, BN));
+  LCE_TRY(map_kmajor(&tb, weight, pl.Vl, pl.D, pl.D, b_box_rows()));
   GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(pl.Vl)};
   EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), static_cast<int32_t>(pl.Vl), pm, ps, pl.cap, zt};
   LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s)));
@@ -477,7 +511,7 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
     const int64_t vc = (pl.Vl - v0) < pl.Vc ? (pl.Vl - v0) : pl.Vc;
     const uint16_t* wc = weight + v0 * pl.D;
     CUtensorMap t_w_k, t_w_mn;
-    LCE_TRY(map_kmajor(&t_w_k, wc, vc, pl.D, pl.D, BN));
+    LCE_TRY(map_kmajor(&t_w_k, wc, vc, pl.D, pl.D, b_box_rows()));
     LCE_TRY(map_mnmajor(&t_w_mn, wc, vc, pl.D, pl.D));
     // S4: recompute logits of the chunk, G_c = softmax - onehot (bf16)
     {
@@ -594,7 +628,7 @@ lce_status_t lce_debug_gemm(const uint16_t* A, const uint16_t* B, float* C, int6
   if (a_mn) LCE_TRY(map_mnmajor(&ta, A, K, M, M));
   else LCE_TRY(map_kmajor(&ta, A, M, K, K, BM));
   if (b_mn) LCE_TRY(map_mnmajor(&tb, B, K, N, N));
-  else LCE_TRY(map_kmajor(&tb, B, N, K, K, BN));
+  else LCE_TRY(map_kmajor(&tb, B, N, K, K, b_box_rows()));
   GemmDims d{nullptr, static_cast<int32_t>(M), nullptr, static_cast<int32_t>(K), static_cast<int32_t>(N)};
   EpiStore::Params ep{C, N};
   if (!a_mn && !b_mn) return launch_gemm<false, false, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);

@@ -14,6 +14,7 @@ from typing import Optional
 import torch
 
 from ._lib import KERNEL_CLASSES, LCE_K_COUNT, Problem, check, lib
+from .dist import broadcast_bytes, shard_range  # noqa: F401
 
 MEAN, SUM = 0, 1
 _RED = {"mean": MEAN, "sum": SUM}
@@ -90,14 +91,14 @@ class Comm:
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
-        obj = [None]
+        payload = None
         if rank == 0:
             buf = ctypes.create_string_buffer(128)
             check(lib.lce_comm_get_unique_id(buf), "lce_comm_get_unique_id")
-            obj = [bytes(buf.raw)]
-        dist.broadcast_object_list(obj, src=0, group=group)
+            payload = bytes(buf.raw)
+        uid = broadcast_bytes(payload, group=group)
         h = ctypes.c_void_p()
-        check(lib.lce_comm_init(ctypes.byref(h), obj[0], world, rank), "lce_comm_init")
+        check(lib.lce_comm_init(ctypes.byref(h), uid, world, rank), "lce_comm_init")
         return cls(h, world, rank)
 
     @classmethod
@@ -113,13 +114,6 @@ class Comm:
         if self.handle:
             check(lib.lce_comm_destroy(self.handle), "lce_comm_destroy")
             self.handle = None
-
-
-def shard_range(vocab: int, world: int, rank: int):
-    """Contiguous vocab shard of `rank` (R19): V_l = ceil(V / P), last shorter."""
-    vl = -(-vocab // world)
-    start = min(vocab, rank * vl)
-    return start, min(vocab, start + vl) - start
 
 
 def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *, ignore_index: int = -100,

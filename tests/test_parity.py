@@ -22,6 +22,13 @@ pytestmark = pytest.mark.gpu
 LOSS_TOL, GRAD_TOL, LSE_TOL = 2e-3, 1e-2, 1e-3
 
 
+@pytest.fixture(params=["pair", "single"])
+def variant(request, monkeypatch):
+    """Both tcgen05 mainloops: CTA pairs (cta_group::2, default) and single CTA."""
+    monkeypatch.setenv("LCE_GEMM", request.param)
+    return request.param
+
+
 def gpu_run(inp, reduction="mean", grad=None, budget=0, comm=None, accumulate_into=None):
     import paper_2605_21442_b200 as F
 
@@ -82,7 +89,7 @@ def assert_parity(g, o, labels, ignore=IGNORE):
 # ------------------------------------------------------------ mainloop descriptors
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (64, 40, 16), (136, 264, 72)])
-def test_debug_gemm_matches_fp64(cuda_lib, a_mn, b_mn, M, N, K):
+def test_debug_gemm_matches_fp64(cuda_lib, variant, a_mn, b_mn, M, N, K):
     """The tcgen05 mainloop (smem/instruction descriptors, TMA swizzle, both
     operand majors, ragged M/N/K tails) computes A B^T."""
     import paper_2605_21442_b200 as F
@@ -102,7 +109,7 @@ def test_debug_gemm_matches_fp64(cuda_lib, a_mn, b_mn, M, N, K):
 # ------------------------------------------------------------ tiny config (full oracle)
 @pytest.mark.parametrize("reduction", ["mean", "sum"])
 @pytest.mark.parametrize("regime", ["random", "confident"])
-def test_tiny_config(cuda_lib, reduction, regime):
+def test_tiny_config(cuda_lib, variant, reduction, regime):
     inp = make_config("tiny", device="cuda", regime=regime)
     g = gpu_run(inp, reduction)
     o = oracle_run(inp, reduction)
@@ -111,7 +118,7 @@ def test_tiny_config(cuda_lib, reduction, regime):
 
 # ------------------------------------------------------------ exact (D, V) of every config, reduced N
 @pytest.mark.parametrize("name", ["llama1b", "llama8b", "qwen7b", "llama70b"])
-def test_config_shapes_reduced_n(cuda_lib, name):
+def test_config_shapes_reduced_n(cuda_lib, variant, name):
     """Each BASELINE config's exact (D, V) (incl. the vocab tail tile) with a
     ragged N spanning several 128-row tiles; 10% ignored rows (qwen: the packed
     label structure)."""
@@ -133,7 +140,7 @@ def small(N, D, V, seed=0, ignore_frac=0.1, labels=None, regime="random"):
 
 
 @pytest.mark.parametrize("N,D,V", [(1, 64, 1000), (127, 64, 257), (129, 72, 256), (200, 8, 513), (260, 136, 2)])
-def test_ragged_shapes(cuda_lib, N, D, V):
+def test_ragged_shapes(cuda_lib, variant, N, D, V):
     inp = small(N, D, V, seed=N)
     assert_parity(gpu_run(inp), oracle_run(inp), inp.labels.cpu().numpy())
 
@@ -146,7 +153,7 @@ def test_single_class_vocab(cuda_lib):
     assert np.abs(g["dH"]).max() <= 1e-6 and np.abs(g["dW"]).max() <= 1e-6
 
 
-def test_empty_and_all_ignored(cuda_lib):
+def test_empty_and_all_ignored(cuda_lib, variant):
     """N = 0 and N_v = 0: loss 0, lse 0, dH 0, dW 0."""
     inp = small(0, 64, 1000)
     g = gpu_run(inp)
@@ -205,7 +212,7 @@ def test_grad_scale_sum_and_accumulate(cuda_lib):
     assert fro_rel(ga["dW"] - base.cpu().double().numpy(), o["dW"]) <= GRAD_TOL
 
 
-def test_chunk_budget_is_not_semantics(cuda_lib):
+def test_chunk_budget_is_not_semantics(cuda_lib, variant):
     """R7: several vocab chunks (tiny budget) give the same result as one."""
     inp = small(384, 128, 3000, seed=4)
     one = gpu_run(inp)
