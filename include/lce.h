@@ -48,7 +48,7 @@ typedef enum {
   LCE_ERR_NULL = 1,        /* required pointer is NULL                         */
   LCE_ERR_SHAPE = 2,       /* N<0, D<=0, D%8!=0, V_l<=0, bad vocab range, >2^31 */
   LCE_ERR_ALIGN = 3,       /* a pointer is not 16-byte aligned                 */
-  LCE_ERR_REDUCTION = 4,   /* reduction is not LCE_MEAN / LCE_SUM              */
+  LCE_ERR_REDUCTION = 4,   /* reduction is not LCE_MEAN / LCE_SUM / LCE_NONE   */
   LCE_ERR_WORKSPACE = 5,   /* workspace_bytes < lce_workspace_bytes(problem)   */
   LCE_ERR_LABEL_RANGE = 6, /* a label outside [0, V_total) that is not ignored */
   LCE_ERR_DEVICE = 7,      /* current device is not sm_100 (B200)              */
@@ -57,7 +57,13 @@ typedef enum {
   LCE_ERR_COMM = 10        /* communicator does not match the problem          */
 } lce_status_t;
 
-typedef enum { LCE_MEAN = 0, LCE_SUM = 1 } lce_reduction_t;
+/* MEAN: L = sum_i loss_i / N_v.  SUM: L = sum_i loss_i.
+ * NONE (per-token, the log-prob interface GRPO/DPO need -- P:322, P:463,
+ * Table 4): the forward's token_loss = -log p(y_i | h_i) is the result and
+ * `loss` receives sum_i loss_i; the backward's grad_loss is a [N] vector of
+ * per-token upstream gradients g_i = dL/dloss_i (NULL = all ones), so
+ * G_ij = g_i (softmax(z_i)_j - [j = y_i]). */
+typedef enum { LCE_MEAN = 0, LCE_SUM = 1, LCE_NONE = 2 } lce_reduction_t;
 
 /* Opaque vocab-parallel communicator (NCCL over NVLink).  NULL = one GPU. */
 typedef struct lce_comm_s* lce_comm_t;
@@ -107,7 +113,8 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm,
  * bounded vocab chunk at a time), then dH += G_c W_c and dW_c = G_c^T H on
  * the tensor cores with fp32 accumulation.
  *   lse        [N] fp32 in: the forward's lse output (same H, W, labels)
- *   grad_loss  [1] fp32 in (device) or NULL for 1.0: g = dL_total/dL
+ *   grad_loss  fp32 in (device) or NULL for 1.0: MEAN / SUM: [1], g = dL_total/dL;
+ *              NONE: [N], g_i = dL_total/dloss_i (ignored rows' entries unused)
  *   dhidden    [N, D] bf16 out: dH (RNE from fp32); rows of ignored tokens 0
  *   dweight    [V_l, D] fp32 out: dW for this rank's rows
  *   accumulate_dweight  0: dweight = dW, 1: dweight += dW

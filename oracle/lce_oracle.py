@@ -28,6 +28,9 @@ Readings of points the paper leaves open (full list in DESIGN.md):
   R5 lse / per-token loss of ignored rows are 0
   R6 natural log
   R11 upstream gradient g (dL/dloss) scales the gradients; default 1
+  R21 reduction "none" (per-token log-probs, the interface GRPO / DPO need,
+      P:322, Table 4): loss_i is the result, `loss` is their sum, and
+      the upstream gradient is a per-token vector g_i
 
 Every function is pinned in tests/test_oracle.py against closed forms, brute
 force, finite differences and torch's CPU fp64 cross-entropy + autograd.
@@ -69,13 +72,20 @@ def _valid_rows(y: np.ndarray, vocab: int, ignore_index: int) -> np.ndarray:
     return valid
 
 
-def _scale(reduction: str, n_valid: int, grad_loss: float) -> float:
-    """c = g (sum) or g / N_v (mean, S:306); 0 if N_v = 0 (S:303)."""
-    if reduction not in ("mean", "sum"):
-        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+def _scale(reduction: str, n_valid: int, grad_loss, rows=None):
+    """c = g (sum) or g / N_v (mean, S:306); 0 if N_v = 0 (S:303).
+    For "none" (R21) the per-row scale g_i of the selected valid rows."""
+    if reduction not in ("mean", "sum", "none"):
+        raise ValueError(f"reduction must be 'mean', 'sum' or 'none', got {reduction!r}")
+    if reduction == "none":
+        if grad_loss is None or np.ndim(grad_loss) == 0:
+            g = 1.0 if grad_loss is None else float(grad_loss)
+            return np.full(0 if rows is None else len(rows), g)
+        return np.asarray(grad_loss, dtype=np.float64)[rows]
+    g = 1.0 if grad_loss is None else float(grad_loss)
     if n_valid == 0:
         return 0.0
-    return float(grad_loss) / n_valid if reduction == "mean" else float(grad_loss)
+    return g / n_valid if reduction == "mean" else g
 
 
 def _log_softmax_stats(z: np.ndarray):
@@ -111,20 +121,20 @@ def lce_forward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
     total = float(tok.sum())                          # step 5
     if reduction == "mean":
         loss = total / n_valid if n_valid else 0.0    # R1, R2
-    elif reduction == "sum":
+    elif reduction in ("sum", "none"):                # "none": token_loss is the result (R21)
         loss = total
     else:
-        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+        raise ValueError(f"reduction must be 'mean', 'sum' or 'none', got {reduction!r}")
     return {"loss": loss, "lse": lse, "token_loss": tok, "n_valid": n_valid}
 
 
 def lce_backward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
-                 reduction: str = "mean", grad_loss: float = 1.0) -> dict:
+                 reduction: str = "mean", grad_loss=1.0) -> dict:
     """Analytic gradients of the loss: dH = G W, dW = G^T H.
 
     G_ij = c (softmax(z_i)_j - [j = y_i]) for valid rows, 0 for ignored rows,
-    with c from ``_scale``.  Returns ``dH`` [N, D], ``dW`` [V, D] (fp64),
-    ``n_valid`` and ``c``.
+    with c from ``_scale`` (for "none": c_i = grad_loss[i], a length-N vector).
+    Returns ``dH`` [N, D], ``dW`` [V, D] (fp64), ``n_valid`` and ``c``.
     """
     H = _as_f64(hidden)
     W = _as_f64(weight)
@@ -133,7 +143,7 @@ def lce_backward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
     valid = _valid_rows(y, V, ignore_index)
     rows = np.flatnonzero(valid)
     n_valid = int(rows.size)
-    c = _scale(reduction, n_valid, grad_loss)          # step 7
+    c = _scale(reduction, n_valid, grad_loss, rows)    # step 7
     dH = np.zeros_like(H)
     dW = np.zeros_like(W)
     if n_valid:
@@ -142,7 +152,7 @@ def lce_backward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
         _, lse = _log_softmax_stats(z)
         G = np.exp(z - lse[:, None])                   # step 8: p_ij
         G[np.arange(n_valid), y[rows]] -= 1.0          #         p - onehot
-        G *= c
+        G *= c if np.ndim(c) == 0 else c[:, None]
         dH[rows] = G @ W                               # step 9
         dW = G.T @ Hv
     return {"dH": dH, "dW": dW, "n_valid": n_valid, "c": c}
@@ -150,7 +160,7 @@ def lce_backward(hidden, weight, labels, ignore_index: int = IGNORE_INDEX,
 
 def lce_rows(hidden, weight, labels, rows, n_valid: int,
              ignore_index: int = IGNORE_INDEX, reduction: str = "mean",
-             grad_loss: float = 1.0) -> dict:
+             grad_loss=1.0) -> dict:
     """Row-local quantities for selected rows only (lse, token loss, dH rows).
 
     Used to check the GPU at sizes where the full oracle is too slow: lse_i,
@@ -163,12 +173,12 @@ def lce_rows(hidden, weight, labels, rows, n_valid: int,
     y = np.asarray(labels, dtype=np.int64)[rows]
     V = W.shape[0]
     valid = _valid_rows(y, V, ignore_index)
-    c = _scale(reduction, n_valid, grad_loss)
     k = rows.size
+    sel = np.flatnonzero(valid)
+    c = _scale(reduction, n_valid, grad_loss, rows[sel])
     lse = np.zeros(k)
     tok = np.zeros(k)
     dH = np.zeros((k, W.shape[1]))
-    sel = np.flatnonzero(valid)
     if sel.size:
         z = H[sel] @ W.T
         _, l = _log_softmax_stats(z)
@@ -176,7 +186,7 @@ def lce_rows(hidden, weight, labels, rows, n_valid: int,
         tok[sel] = l - z[np.arange(sel.size), y[sel]]
         G = np.exp(z - l[:, None])
         G[np.arange(sel.size), y[sel]] -= 1.0
-        dH[sel] = c * (G @ W)
+        dH[sel] = (c if np.ndim(c) == 0 else c[:, None]) * (G @ W)
     return {"lse": lse, "token_loss": tok, "dH": dH}
 
 

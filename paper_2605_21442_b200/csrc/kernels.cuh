@@ -100,12 +100,14 @@ struct EpiG {
     int32_t n_cols;       // valid columns of this chunk
     uint16_t* G;          // [rows_cap][ldg] bf16
     int64_t ldg;
+    const float* row_scale;  // [N_v] per-token upstream gradient (reduction NONE) or null
   };
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;
     const float lsel = valid ? p.lse_c[r] * kLog2e : 0.f;
+    const float rs = (valid && p.row_scale) ? p.row_scale[r] : 1.f;
     uint4* dst = reinterpret_cast<uint4*>(p.G + static_cast<int64_t>(r) * p.ldg + t.n0);
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
@@ -117,8 +119,8 @@ struct EpiG {
       for (int j = 0; j < 32; j += 2) {
         float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c * 32 + j == yl ? 1.f : 0.f);
         float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c * 32 + j + 1 == yl ? 1.f : 0.f);
-        if (!valid || cb + j >= p.n_cols) g0 = 0.f;
-        if (!valid || cb + j + 1 >= p.n_cols) g1 = 0.f;
+        g0 = (!valid || cb + j >= p.n_cols) ? 0.f : g0 * rs;
+        g1 = (!valid || cb + j + 1 >= p.n_cols) ? 0.f : g1 * rs;
         w[j / 2] = pack_bf16x2(g0, g1);
       }
 #pragma unroll
@@ -249,6 +251,7 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
                                                     float* __restrict__ lse_out, float* __restrict__ tok_out,
                                                     Header* hdr, const float* __restrict__ grad_loss,
                                                     int reduction) {
+  // grad_loss is a device scalar for MEAN / SUM and ignored for NONE
   __shared__ int warp_tot[32];
   __shared__ int base_s;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -318,8 +321,9 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
     hdr->status = any_bad ? kStatusBadLabel : 0u;
     const int nv = base_s;
     hdr->n_valid = nv;
-    const float g = grad_loss ? *grad_loss : 1.f;
-    hdr->c = nv == 0 ? 0.f : (reduction == 0 ? g / static_cast<float>(nv) : g);
+    const float g = (grad_loss && reduction != 2) ? *grad_loss : 1.f;
+    // MEAN: g / N_v, SUM: g, NONE: 1 (per-token upstream grads are folded into G)
+    hdr->c = nv == 0 ? 0.f : (reduction == 0 ? g / static_cast<float>(nv) : (reduction == 1 ? g : 1.f));
     hdr->counter = 0u;
   }
 }
@@ -332,7 +336,8 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
 __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict__ H, int64_t D, int N,
                                                      const int32_t* __restrict__ idx, const Header* hdr,
                                                      uint16_t* __restrict__ Hc, const float* __restrict__ lse_in,
-                                                     float* __restrict__ lse_c, const int32_t* __restrict__ y,
+                                                     float* __restrict__ lse_c, const float* __restrict__ grad_in,
+                                                     float* __restrict__ grad_c, const int32_t* __restrict__ y,
                                                      int32_t ignore, int64_t vocab_total,
                                                      uint16_t* __restrict__ dhidden) {
   const int b = blockIdx.x;
@@ -344,6 +349,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict_
     const uint4* src = reinterpret_cast<const uint4*>(H + static_cast<int64_t>(src_row) * D);
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
     if (lse_in && threadIdx.x == 0) lse_c[b] = lse_in[src_row];
+    if (grad_in && threadIdx.x == 0) grad_c[b] = grad_in[src_row];
   } else if (b < ((nv + 127) & ~127)) {
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
   }

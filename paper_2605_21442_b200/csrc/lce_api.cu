@@ -40,7 +40,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // ------------------------------------------------------------------ workspace plan
 struct Plan {
   int64_t N, D, Vl, cap, n_tiles, Vc, n_chunks, nblocks;
-  size_t hdr, idx, yc, zt, lsec, bsum, mloc, mglob, sbuf, hc, region, pm, ps, g, dh, total;
+  size_t hdr, idx, yc, zt, lsec, gsc, bsum, mloc, mglob, sbuf, hc, region, pm, ps, g, dh, total;
 };
 
 bool make_plan(const lce_problem_t* p, Plan* pl) {
@@ -73,6 +73,7 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.yc = take(q.cap * 4);
   q.zt = take(q.cap * 4);
   q.lsec = take(q.cap * 4);
+  q.gsc = take(q.cap * 4);
   q.bsum = take(q.nblocks * 8);
   q.mloc = take(q.cap * 4);
   q.mglob = take(q.cap * 4);
@@ -308,6 +309,8 @@ NcclApi* nccl() {
 struct lce_comm_s {
   ncclComm_t comm;
   int nranks, rank;
+  cudaStream_t side;          // runs the dH all-reduce concurrently with the last dW GEMM
+  cudaEvent_t dh_ready, dh_reduced;
 };
 
 namespace {
@@ -322,7 +325,7 @@ lce_status_t allreduce(lce_comm_t c, void* buf, size_t count, ncclRedOp_t op, cu
 
 lce_status_t validate(const lce_problem_t* p, lce_comm_t comm, size_t ws_bytes, const void* ws, Plan* pl) {
   if (!p) return LCE_ERR_NULL;
-  if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM) return LCE_ERR_REDUCTION;
+  if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   if (!make_plan(p, pl)) return LCE_ERR_SHAPE;
   if (!ws) return LCE_ERR_NULL;
   if (!aligned16(ws)) return LCE_ERR_ALIGN;
@@ -411,7 +414,8 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
   {  // S0: gather valid rows of H
     LaunchScope sc(LCE_K_GATHER, s);
     gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, nullptr, nullptr,
-                                                               labels, p->ignore_index, p->vocab_total, nullptr);
+                                                               nullptr, nullptr, labels, p->ignore_index,
+                                                               p->vocab_total, nullptr);
     LCE_TRY(last_error());
   }
   // S1+S2: logits tile by tile in TMEM, online LSE epilogue
@@ -483,6 +487,9 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
   int32_t* yc = reinterpret_cast<int32_t*>(ws + pl.yc);
   float* zt = reinterpret_cast<float*>(ws + pl.zt);
   float* lsec = reinterpret_cast<float*>(ws + pl.lsec);
+  float* gsc = reinterpret_cast<float*>(ws + pl.gsc);
+  // reduction NONE: grad_loss is [N] per-token upstream gradients, folded into G per row
+  const float* row_grad = p->reduction == LCE_NONE ? grad_loss : nullptr;
   uint16_t* hc = reinterpret_cast<uint16_t*>(ws + pl.hc);
   uint16_t* G = reinterpret_cast<uint16_t*>(ws + pl.g);
   float* dh = reinterpret_cast<float*>(ws + pl.dh);
@@ -496,8 +503,8 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
   }
   {
     LaunchScope sc(LCE_K_GATHER, s);
-    gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, lse, lsec, labels,
-                                                               p->ignore_index, p->vocab_total, dhidden);
+    gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, lse, lsec, row_grad,
+                                                               gsc, labels, p->ignore_index, p->vocab_total, dhidden);
     LCE_TRY(last_error());
   }
   CUtensorMap t_hc_k, t_hc_mn, t_g_k, t_g_mn;
@@ -516,7 +523,8 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
     // S4: recompute logits of the chunk, G_c = softmax - onehot (bf16)
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(vc)};
-      EpiG::Params ep{yc, lsec, static_cast<int32_t>(p->vocab_start + v0), static_cast<int32_t>(vc), G, pl.Vc};
+      EpiG::Params ep{yc, lsec, static_cast<int32_t>(p->vocab_start + v0), static_cast<int32_t>(vc), G, pl.Vc,
+                      row_grad ? gsc : nullptr};
       LCE_TRY((launch_gemm<false, false, EpiG>(LCE_K_BWD_G, t_hc_k, t_w_k, d, ep, dev.sms, s)));
     }
     // S6: dH (+)= G_c W_c   (A = G_c K-major over vocab, B = W_c MN-major)
@@ -524,6 +532,15 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
       EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx};
       LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
+    }
+    // S7 (vocab-parallel): once the last chunk's dH partial is complete, its
+    // all-reduce runs on the communicator's side stream while the last dW GEMM
+    // (which does not read dH) runs here.
+    if (multi && k == pl.n_chunks - 1) {
+      LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
+      LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
+      LCE_TRY(allreduce(comm, dh, static_cast<size_t>(pl.N * pl.D), ncclSum, comm->side));
+      LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
     }
     // S5: dW_c = c G_c^T H   (A = G_c MN-major, B = H_c MN-major, K = N_v)
     {
@@ -534,7 +551,7 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
   }
   if (multi) {
     // S7: dH summed over the vocab shards, then scaled, cast, scattered
-    LCE_TRY(allreduce(comm, dh, static_cast<size_t>(pl.N * pl.D), ncclSum, s));
+    LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
     LaunchScope sc(LCE_K_FINAL, s);
     finalize_dh_kernel<<<static_cast<unsigned>(pl.N), 256, 0, s>>>(dh, pl.D, idx, hdr, dhidden);
     LCE_TRY(last_error());
@@ -572,7 +589,15 @@ lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, 
   memcpy(&u, id, 128);
   ncclComm_t c;
   if (api->commInitRank(&c, nranks, u, rank) != ncclSuccess) return LCE_ERR_NCCL;
-  *comm = new lce_comm_s{c, nranks, rank};
+  lce_comm_s* cs = new lce_comm_s{c, nranks, rank, nullptr, nullptr, nullptr};
+  if (cudaStreamCreateWithFlags(&cs->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&cs->dh_ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&cs->dh_reduced, cudaEventDisableTiming) != cudaSuccess) {
+    api->commDestroy(c);
+    delete cs;
+    return LCE_ERR_CUDA;
+  }
+  *comm = cs;
   return LCE_OK;
 }
 
@@ -581,6 +606,9 @@ lce_status_t lce_comm_destroy(lce_comm_t comm) {
   NcclApi* api = nccl();
   lce_status_t st = LCE_OK;
   if (api && api->commDestroy(comm->comm) != ncclSuccess) st = LCE_ERR_NCCL;
+  if (comm->side) cudaStreamDestroy(comm->side);
+  if (comm->dh_ready) cudaEventDestroy(comm->dh_ready);
+  if (comm->dh_reduced) cudaEventDestroy(comm->dh_reduced);
   delete comm;
   return st;
 }

@@ -16,8 +16,8 @@ import torch
 from ._lib import KERNEL_CLASSES, LCE_K_COUNT, Problem, check, lib
 from .dist import broadcast_bytes, shard_range  # noqa: F401
 
-MEAN, SUM = 0, 1
-_RED = {"mean": MEAN, "sum": SUM}
+MEAN, SUM, NONE = 0, 1, 2
+_RED = {"mean": MEAN, "sum": SUM, "none": NONE}
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -33,7 +33,7 @@ def make_problem(n_tokens: int, hidden_dim: int, vocab_local: int, *, vocab_star
                  vocab_total: Optional[int] = None, ignore_index: int = -100, reduction: str = "mean",
                  chunk_budget_bytes: int = 0) -> Problem:
     if reduction not in _RED:
-        raise ValueError(f"reduction must be 'mean' or 'sum', got {reduction!r}")
+        raise ValueError(f"reduction must be 'mean', 'sum' or 'none', got {reduction!r}")
     return Problem(n_tokens, hidden_dim, vocab_local, vocab_start,
                    vocab_local if vocab_total is None else vocab_total, ignore_index, _RED[reduction],
                    chunk_budget_bytes)
@@ -120,7 +120,11 @@ def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *,
             reduction: str = "mean", comm: Optional[Comm] = None, vocab_start: int = 0,
             vocab_total: Optional[int] = None, with_token_loss: bool = False, workspace: Optional[Workspace] = None,
             chunk_budget_bytes: int = 0, stream=None, out: Optional[dict] = None) -> dict:
-    """loss [1] fp32, lse [N] fp32 (0 on ignored rows), n_valid [1] int32, token_loss."""
+    """loss [1] fp32, lse [N] fp32 (0 on ignored rows), n_valid [1] int32, token_loss.
+
+    reduction 'none' returns the per-token losses (-log p(y_i)) in token_loss
+    and their sum in loss."""
+    with_token_loss = with_token_loss or reduction == "none"
     _check_inputs(hidden, weight, labels)
     N, D = hidden.shape
     prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
@@ -146,7 +150,9 @@ def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, l
              dhidden: Optional[torch.Tensor] = None, dweight: Optional[torch.Tensor] = None,
              accumulate_dweight: bool = False, workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0,
              stream=None):
-    """dhidden [N, D] bf16 and dweight [V_l, D] fp32 (overwritten or accumulated)."""
+    """dhidden [N, D] bf16 and dweight [V_l, D] fp32 (overwritten or accumulated).
+
+    grad_loss: scalar dL/dloss for 'mean'/'sum'; [N] per-token dL/dloss_i for 'none'."""
     _check_inputs(hidden, weight, labels)
     N, D = hidden.shape
     prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
@@ -159,6 +165,8 @@ def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, l
         dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
     if grad_loss is not None:
         grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+        if grad_loss.numel() != (N if reduction == "none" else 1):
+            raise ValueError("grad_loss must have N elements for 'none' and 1 otherwise")
     check(lib.lce_backward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
                            _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(dweight),
                            1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)), "lce_backward")
@@ -181,13 +189,15 @@ class LinearCrossEntropyFunction(torch.autograd.Function):
         out = forward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)
         ctx.save_for_backward(hidden, weight, labels, out["lse"])
         ctx.cfg = (ignore_index, reduction)
+        if reduction == "none":
+            return out["token_loss"]  # per-token -log p(y_i); 0 on ignored rows
         return out["loss"].reshape(())
 
     @staticmethod
     def backward(ctx, g):
         hidden, weight, labels, lse = ctx.saved_tensors
         ignore_index, reduction = ctx.cfg
-        dh, dw = backward(hidden, weight, labels, lse, grad_loss=g.reshape(1), ignore_index=ignore_index,
+        dh, dw = backward(hidden, weight, labels, lse, grad_loss=g.reshape(-1), ignore_index=ignore_index,
                           reduction=reduction)
         return dh, dw.to(weight.dtype), None, None, None
 

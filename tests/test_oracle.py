@@ -363,3 +363,35 @@ def test_vocab_shard_statistics_combine_to_global(P):
     f = lce_forward(H, W, y)
     np.testing.assert_allclose(comb["lse"], f["lse"], rtol=1e-14, atol=1e-14)
     np.testing.assert_allclose(comb["token_loss"], f["token_loss"], rtol=1e-12, atol=1e-13)
+
+
+# ---------------------------------------------------------------- reduction "none" (R21)
+def test_none_reduction_matches_torch_per_token_and_vector_grad():
+    """R21 / P10: per-token losses equal torch CE(reduction='none'); the
+    gradient of sum_i g_i loss_i equals torch autograd with grad vector g."""
+    H, W, y = rand_problem(80, 12, 200, 17, ignore_frac=0.2)
+    g = np.random.default_rng(3).standard_normal(80)
+    Ht = torch.tensor(H, requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    lv = torch.nn.functional.cross_entropy(Ht @ Wt.T, torch.tensor(y), ignore_index=IGNORE_INDEX,
+                                           reduction="none")
+    lv.backward(torch.tensor(g))
+    f = lce_forward(H, W, y, reduction="none")
+    b = lce_backward(H, W, y, reduction="none", grad_loss=g)
+    np.testing.assert_allclose(f["token_loss"], lv.detach().numpy(), rtol=1e-12, atol=1e-14)
+    assert f["loss"] == pytest.approx(lv.sum().item(), rel=1e-12)
+    np.testing.assert_allclose(b["dH"], Ht.grad.numpy(), rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(b["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-14)
+    rows = np.array([1, 7, 40])
+    r = lce_rows(H, W, y, rows, n_valid=f["n_valid"], reduction="none", grad_loss=g)
+    np.testing.assert_allclose(r["dH"], b["dH"][rows], rtol=1e-13, atol=1e-16)
+
+
+def test_none_with_uniform_weights_is_mean():
+    """P8 for R21: g_i = 1/N_v on every token reproduces the MEAN gradients."""
+    H, W, y = rand_problem(50, 6, 30, 18)
+    nv = int((y != IGNORE_INDEX).sum())
+    bn = lce_backward(H, W, y, reduction="none", grad_loss=np.full(50, 1.0 / nv))
+    bm = lce_backward(H, W, y, reduction="mean")
+    np.testing.assert_allclose(bn["dH"], bm["dH"], rtol=1e-13, atol=1e-17)
+    np.testing.assert_allclose(bn["dW"], bm["dW"], rtol=1e-13, atol=1e-17)

@@ -278,6 +278,43 @@ def test_autograd_function(cuda_lib):
     assert fro_rel(w.grad.float().cpu().double().numpy(), o["dW"]) <= 2e-2  # dW rounded to bf16 for autograd
 
 
+@pytest.mark.parametrize("N,D,V", [(300, 128, 3000), (257, 4096, 128256)])
+def test_none_reduction_per_token_logprobs(cuda_lib, variant, N, D, V):
+    """R21 (GRPO / DPO token log-probs): per-token losses and
+    the backward of sum_i g_i loss_i for an arbitrary upstream vector g."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(N, D, V, seed=9)
+    g = torch.randn(N, generator=torch.Generator().manual_seed(1)).float()
+    out = F.forward(inp.hidden, inp.weight, inp.labels, reduction="none")
+    dh, dw = F.backward(inp.hidden, inp.weight, inp.labels, out["lse"], grad_loss=g.cuda(), reduction="none")
+    torch.cuda.synchronize()
+    H, W, y = np_inputs(inp)
+    f = lce_forward(H, W, y, reduction="none")
+    b = lce_backward(H, W, y, reduction="none", grad_loss=g.double().numpy())
+    tok = out["token_loss"].cpu().double().numpy()
+    assert np.abs(tok - f["token_loss"]).max() <= LSE_TOL * np.abs(f["lse"]).max()
+    assert abs(out["loss"].item() - f["loss"]) <= LOSS_TOL * abs(f["loss"])
+    assert fro_rel(dh.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
+    assert fro_rel(dw.cpu().double().numpy(), b["dW"]) <= GRAD_TOL
+    assert np.all(dh.float().cpu().numpy()[y == IGNORE] == 0)
+
+
+def test_autograd_none_reduction(cuda_lib):
+    import paper_2605_21442_b200 as F
+
+    inp = small(200, 64, 1000, seed=10)
+    h = inp.hidden.clone().requires_grad_(True)
+    w = inp.weight.clone().requires_grad_(True)
+    tok = F.linear_cross_entropy(h, w, inp.labels, reduction="none")
+    assert tok.shape == (200,)
+    g = torch.linspace(-1, 1, 200, device="cuda")
+    (tok * g).sum().backward()
+    H, W, y = np_inputs(inp)
+    b = lce_backward(H, W, y, reduction="none", grad_loss=g.double().cpu().numpy())
+    assert fro_rel(h.grad.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
+
+
 # ------------------------------------------------------------ full size, bench launch configuration
 @pytest.mark.parametrize("name", ["llama8b", "qwen7b"])
 def test_full_size_sampled_rows_and_invariants(cuda_lib, name):
