@@ -182,6 +182,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chunk-budget", type=int, default=0,
+                    help="chunk_budget_bytes (fused: logit+G chunk bytes, default 4 GiB; split: G chunk, 512 MiB)")
+    ap.add_argument("--path", default="auto", choices=["auto", "fused", "split"],
+                    help="fused = lce_forward_backward (no recompute, 1 GPU); split = lce_forward + lce_backward "
+                         "(recompute; vocab-parallel); auto = fused on 1 GPU, split otherwise")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,10 +224,20 @@ def main():
     dH = torch.empty_like(H)
     dW = torch.empty(vl, D, dtype=torch.float32, device=dev)
 
+    fused = args.path == "fused" or (args.path == "auto" and world == 1)
+
+    def run_path(Hx, Wx, yx):
+        if fused:  # lce_forward_backward: logits kept per row chunk, 6 N_v V D flops
+            F.forward_backward(Hx, Wx, yx, dhidden=dH, dweight=dW, workspace=ws, out=out,
+                               chunk_budget_bytes=args.chunk_budget)
+        else:      # lce_forward + lce_backward: recompute from lse, 8 N_v V D flops
+            F.forward(Hx, Wx, yx, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out,
+                      chunk_budget_bytes=args.chunk_budget)
+            F.backward(Hx, Wx, yx, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH,
+                       dweight=dW, workspace=ws, chunk_budget_bytes=args.chunk_budget)
+
     def step():
-        F.forward(H, W, y, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out)
-        F.backward(H, W, y, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH, dweight=dW,
-                   workspace=ws)
+        run_path(H, W, y)
 
     torch.cuda.reset_peak_memory_stats(dev)
     for _ in range(args.warmup):
@@ -256,12 +271,13 @@ def main():
     ms_step = ms / args.steps
     value = nv * args.steps / (ms / 1e3)
     sus, burst, hbm, src = peaks()
-    flops_step = 8.0 * nv * V * D
+    flops_step = (6.0 if fused else 8.0) * nv * V * D  # executed tensor-core flops per step
     tensor_frac = flops_step / (ms_step / 1e3) / (sus * 1e12 * world)
 
     # dominant kernel (by device time inside the timed region, on the launching stream)
-    gemm_flops = {"fwd_gemm": 2.0 * nv * vl * D, "bwd_g": 2.0 * nv * vl * D, "bwd_dh": 2.0 * nv * vl * D,
-                  "bwd_dw": 2.0 * nv * vl * D}
+    gemm_flops = {"fwd_gemm": 2.0 * nv * vl * D, "bwd_dh": 2.0 * nv * vl * D, "bwd_dw": 2.0 * nv * vl * D}
+    if not fused:
+        gemm_flops["bwd_g"] = 2.0 * nv * vl * D  # the recompute GEMM (fused: an HBM-bound fix-up kernel)
     dom = max(prof, key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom]
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in prof.items()
@@ -292,9 +308,7 @@ def main():
             Hd.copy_(Hh, non_blocking=True)
             Wd.copy_(Wh, non_blocking=True)
             yd.copy_(yh, non_blocking=True)
-            F.forward(Hd, Wd, yd, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out)
-            F.backward(Hd, Wd, yd, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH, dweight=dW,
-                       workspace=ws)
+            run_path(Hd, Wd, yd)
             lossh.copy_(out["loss"], non_blocking=True)
 
         e2e_step()
@@ -330,7 +344,10 @@ def main():
             "config": {"workload": workload_name(args.config), "N": N, "N_valid": nv, "D": D, "V": V,
                        "parallelism": f"vocab-parallel x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (W alone is %.2f GB > 126 MB); no flush" % (V * D * 2 / 1e9)},
-            "tensor_frac": tensor_frac, "tensor_frac_note": f"8*N_v*V*D per step / (time x {src} sustained bf16 peak x GPUs)",
+            "path": "fused lce_forward_backward" if fused else "lce_forward + lce_backward",
+            "flops_per_step": flops_step,
+            "tensor_frac": tensor_frac,
+            "tensor_frac_note": f"{'6' if fused else '8'}*N_v*V*D executed flops per step / (time x {src} sustained bf16 peak x GPUs)",
             "peak_hbm_bytes": peak_hbm, "naive_logits_bytes_fp32": N * V * 4,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,

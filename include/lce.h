@@ -127,6 +127,55 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm,
                           float* dweight, int accumulate_dweight,
                           void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- optimizer-in-backward for the LM head (Sec. 4.1) -----------
+ * AdamW hyper-parameters (torch.optim.AdamW convention); `step` is
+ * the 1-based count of this update (bias corrections 1 - beta^step). */
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;
+  int64_t step;
+} lce_adamw_t;
+
+/* lce_backward whose dW is consumed by an AdamW step inside the dW GEMM
+ * epilogue, the moment each dW row block is final ("the gradient can then be
+ * released without being retained"): no dW buffer exists.
+ *   weight        [V_l, D] bf16 in/out: read by the GEMMs, then rewritten as
+ *                 bf16(master_weight) row block by row block (each block is
+ *                 rewritten only after every GEMM that reads it)
+ *   master_weight [V_l, D] fp32 in/out (theta); exp_avg / exp_avg_sq [V_l, D]
+ *                 fp32 in/out (m, v)
+ * Other arguments as lce_backward.  The result equals lce_backward (dW) then
+ * one AdamW step on (master_weight, dW) -- P:147's K = 1 equivalence.
+ * LCE_ERR_SHAPE for hyper-parameters outside their domain. */
+lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
+                                const uint16_t* hidden, uint16_t* weight,
+                                const int32_t* labels, const float* lse,
+                                const float* grad_loss, uint16_t* dhidden,
+                                float* master_weight, float* exp_avg,
+                                float* exp_avg_sq, const lce_adamw_t* hp,
+                                void* workspace, size_t workspace_bytes,
+                                void* stream);
+
+/* ---- fused forward + backward (one GPU) ------------------------------------
+ * The same results as lce_forward followed by lce_backward (loss, lse,
+ * token_loss, n_valid, dhidden, dweight; same argument meanings), computed
+ * without recomputing the logits: P:166's "processes hidden states in
+ * chunks" taken literally -- for each chunk of Nc compacted rows the fp32
+ * logits z = H_c W^T are kept (in the workspace, Nc x V_l x 4 bytes, never
+ * N x V_l), reduced to lse, turned into G in place and consumed by the dH and
+ * dW GEMMs: 6 N_v V D flops instead of 8.  The upstream gradient must be
+ * known up front (grad_loss as in lce_backward; NULL = 1).  dW is accumulated
+ * across row chunks in fp32.  Nc is set by chunk_budget_bytes (bytes of the
+ * fp32 + bf16 chunk buffers; 0 = 4 GiB).  comm must be NULL
+ * (LCE_ERR_COMM otherwise): vocab-parallel runs use lce_forward/lce_backward. */
+size_t lce_fused_workspace_bytes(const lce_problem_t* p);
+lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
+                                  const uint16_t* hidden, const uint16_t* weight,
+                                  const int32_t* labels, const float* grad_loss,
+                                  float* loss, float* lse, float* token_loss,
+                                  int32_t* n_valid, uint16_t* dhidden, float* dweight,
+                                  int accumulate_dweight, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* Synchronises `stream`, reads the status word of `workspace` and returns
  * LCE_ERR_LABEL_RANGE if the most recent lce_forward / lce_backward that used
  * this workspace saw a bad label, LCE_OK otherwise.  Every call rewrites the

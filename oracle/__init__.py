@@ -15,4 +15,5 @@ from .lce_oracle import (  # noqa: F401
     shard_stats,
     shard_backward,
     combine_shard_stats,
+    adamw_step,
 )

@@ -50,6 +50,7 @@ __all__ = [
     "shard_stats",
     "shard_backward",
     "combine_shard_stats",
+    "adamw_step",
 ]
 
 
@@ -245,6 +246,26 @@ def shard_backward(hidden, weight_shard, labels, vocab_start: int, lse, c: float
         dH[rows] = G @ Wr
         dW = G.T @ H[rows]
     return {"dH_partial": dH, "dW_shard": dW}
+
+
+def adamw_step(theta, grad, exp_avg, exp_avg_sq, step: int, lr: float, beta1: float = 0.9,
+               beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0):
+    """One AdamW update in fp64 (the torch.optim.AdamW convention).
+
+    Sec. 4.1: the in-backward optimizer applies exactly this per
+    parameter as soon as its gradient is final.  Decoupled decay first:
+    theta <- theta (1 - lr wd); m <- b1 m + (1 - b1) g; v <- b2 v + (1 - b2) g^2;
+    theta <- theta - lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps).
+    Returns (theta, m, v) as new arrays.
+    """
+    th = _as_f64(theta) * (1.0 - lr * weight_decay)
+    g = _as_f64(grad)
+    m = beta1 * _as_f64(exp_avg) + (1.0 - beta1) * g
+    v = beta2 * _as_f64(exp_avg_sq) + (1.0 - beta2) * g * g
+    bc1 = 1.0 - beta1 ** step
+    bc2 = 1.0 - beta2 ** step
+    th = th - lr * (m / bc1) / (np.sqrt(v / bc2) + eps)
+    return th, m, v
 
 
 def combine_shard_stats(stats: list) -> dict:

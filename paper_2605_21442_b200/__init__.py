@@ -11,9 +11,12 @@ from .lce import (  # noqa: F401
     LinearCrossEntropyFunction,
     Workspace,
     backward,
+    backward_adamw,
     check_device_status,
     debug_gemm,
     forward,
+    forward_backward,
+    fused_workspace_bytes,
     launch_count,
     linear_cross_entropy,
     make_problem,

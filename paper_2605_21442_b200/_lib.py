@@ -24,8 +24,13 @@ EXPORTS = [
     "lce_workspace_bytes", "lce_forward", "lce_backward", "lce_check_device_status",
     "lce_comm_get_unique_id", "lce_comm_init", "lce_comm_destroy", "lce_comm_size", "lce_comm_rank",
     "lce_status_string", "lce_abi_version", "lce_launch_count", "lce_profile_enable", "lce_profile_read",
-    "lce_debug_gemm",
+    "lce_debug_gemm", "lce_fused_workspace_bytes", "lce_forward_backward", "lce_backward_adamw",
 ]
+
+
+class AdamW(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float), ("weight_decay", ctypes.c_float), ("step", ctypes.c_int64)]
 
 
 class LceError(RuntimeError):
@@ -50,7 +55,7 @@ class Problem(ctypes.Structure):
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2605_21442_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2605_21442_b200/build.py` "
             "(there is deliberately no fallback implementation)")
     lib = ctypes.CDLL(LIB_PATH)
     P = ctypes.POINTER
@@ -61,6 +66,14 @@ def _load() -> ctypes.CDLL:
     lib.lce_forward.restype = ctypes.c_int
     lib.lce_backward.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, ctypes.c_size_t, vp]
     lib.lce_backward.restype = ctypes.c_int
+    lib.lce_fused_workspace_bytes.argtypes = [P(Problem)]
+    lib.lce_fused_workspace_bytes.restype = ctypes.c_size_t
+    lib.lce_forward_backward.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp,
+                                         ctypes.c_size_t, vp]
+    lib.lce_forward_backward.restype = ctypes.c_int
+    lib.lce_backward_adamw.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, P(AdamW), vp,
+                                       ctypes.c_size_t, vp]
+    lib.lce_backward_adamw.restype = ctypes.c_int
     lib.lce_check_device_status.argtypes = [vp, vp]
     lib.lce_check_device_status.restype = ctypes.c_int
     lib.lce_comm_get_unique_id.argtypes = [ctypes.c_char_p]

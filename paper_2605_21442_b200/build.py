@@ -1,6 +1,9 @@
 """Builds liblce.so (the C-ABI CUDA library) in-tree for sm_100a with nvcc.
 
-    python -m paper_2605_21442_b200.build [--verbose]
+    python paper_2605_21442_b200/build.py [--verbose]
+
+Run by file path (it must not import the package, whose __init__ loads the
+library this builds); __graft_entry__.build() loads it the same way.
 
 No torch extension machinery: the library is a plain shared object with an
 extern "C" interface (include/lce.h), loaded by the ctypes binding.

@@ -43,6 +43,12 @@ struct GemmDims {
   const int32_t* k_dev;
   int32_t k_static;
   int32_t n;
+  // device extents are clamp(*dev - off, 0, cap) (cap 0 = no upper clamp): a
+  // row chunk [off, off + cap) of the N_v compacted tokens
+  int32_t m_off, m_cap, k_off, k_cap;
+  // split-K: each output tile is computed as `ksplit` (<= 1: one) independent
+  // k-ranges; the epilogue sees the split index and must reduce them itself
+  int32_t ksplit;
 };
 
 // Geometry handed to the epilogue for one output tile.
@@ -50,10 +56,20 @@ struct TileInfo {
   int m0, n0, n_blk;
   int M, N;
   int row;        // row of this thread inside the tile (== TMEM lane)
-  bool zero_acc;  // K == 0: the accumulator was never written, treat as 0
+  bool zero_acc;  // empty k-range: the accumulator was never written, treat as 0
+  int split;      // split-K index of this work item
 };
 
-__device__ __forceinline__ int dev_or(const int32_t* p, int32_t v) { return p ? *p : v; }
+// One work item of the persistent schedule: output tile (mb, nb) and its k-block range.
+struct WorkItem {
+  int mb, nb, s, kb0, kb1;
+};
+
+__device__ __forceinline__ int extent(const int32_t* p, int32_t v, int32_t off, int32_t cap) {
+  int x = p ? *p - off : v;
+  x = x < 0 ? 0 : x;
+  return (cap > 0 && x > cap) ? cap : x;
+}
 
 __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
   const int per_group = kGroupM * num_n;
@@ -63,6 +79,16 @@ __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& m_blk,
   const int r = t - g * per_group;
   m_blk = first_m + r % gsz;
   n_blk = r / gsz;
+}
+
+__device__ __forceinline__ WorkItem work_of(int t, int num_m, int num_n, int S, int num_k) {
+  WorkItem w;
+  const int tile = t / S;
+  w.s = t - tile * S;
+  tile_of(tile, num_m, num_n, w.mb, w.nb);
+  w.kb0 = static_cast<int>(static_cast<long long>(num_k) * w.s / S);
+  w.kb1 = static_cast<int>(static_cast<long long>(num_k) * (w.s + 1) / S);
+  return w;
 }
 
 template <bool A_MN, bool B_MN, class Epi>
@@ -82,13 +108,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  const int M = dev_or(dims.m_dev, dims.m_static);
-  const int K = dev_or(dims.k_dev, dims.k_static);
+  const int M = extent(dims.m_dev, dims.m_static, dims.m_off, dims.m_cap);
+  const int K = extent(dims.k_dev, dims.k_static, dims.k_off, dims.k_cap);
   const int N = dims.n;
   const int num_m = (M + BM - 1) / BM;
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
-  const int num_tiles = num_m * num_n;
+  const int S = dims.ksplit > 1 ? dims.ksplit : 1;
+  const int num_tiles = num_m * num_n * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -118,10 +145,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        int mb, nb;
-        tile_of(t, num_m, num_n, mb, nb);
-        const int m0 = mb * BM, n0 = nb * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const int m0 = w.mb * BM, n0 = w.nb * BN;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], kAStageBytes + kBStageBytes);
           uint8_t* a = sA + stage * kAStageBytes;
@@ -155,10 +181,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * kAStageBytes);
@@ -169,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
             const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
                                      : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
-            mma_bf16_ss(d, ad, bd, idesc, (kb | kk) != 0);
+            mma_bf16_ss(d, ad, bd, idesc, (kb != w.kb0 || kk != 0) ? 1u : 0u);
           }
           mma_commit(&empty[stage]);  // frees the smem slot once these MMAs retire
           if (++stage == kStages) {
@@ -177,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        if (num_k > 0) {
+        if (w.kb1 > w.kb0) {
           mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
         } else {
           mbar_arrive(&tfull[acc]);
@@ -192,12 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      int mb, nb;
-      tile_of(t, num_m, num_n, mb, nb);
+      const WorkItem w = work_of(t, num_m, num_n, S, num_k);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      TileInfo ti{mb * BM, nb * BN, nb, M, N, q * 32 + lane, num_k == 0};
+      TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s};
       Epi::apply(ep, taddr, ti);
       tc_fence_before();
       __syncwarp();
@@ -252,13 +278,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x >> 1;
   const int nclusters = gridDim.x >> 1;
 
-  const int M = dev_or(dims.m_dev, dims.m_static);
-  const int K = dev_or(dims.k_dev, dims.k_static);
+  const int M = extent(dims.m_dev, dims.m_static, dims.m_off, dims.m_cap);
+  const int K = extent(dims.k_dev, dims.k_static, dims.k_off, dims.k_cap);
   const int N = dims.n;
   const int num_m = (M + kPairBM - 1) / kPairBM;
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
-  const int num_tiles = num_m * num_n;
+  const int S = dims.ksplit > 1 ? dims.ksplit : 1;
+  const int num_tiles = num_m * num_n * S;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -288,11 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        int mb, nb;
-        tile_of(t, num_m, num_n, mb, nb);
-        const int ma = mb * kPairBM + 128 * rank;  // this CTA's A rows
-        const int nbh = nb * BN + 128 * rank;      // this CTA's B rows (N half)
-        for (int kb = 0; kb < num_k; ++kb) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const int ma = w.mb * kPairBM + 128 * rank;  // this CTA's A rows
+        const int nbh = w.nb * BN + 128 * rank;      // this CTA's B rows (N half)
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
           uint8_t* a = sA + stage * kHalf;
@@ -326,10 +352,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * kHalf);
@@ -340,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
             const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
                                      : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
-            mma_bf16_ss_pair(d, ad, bd, idesc, (kb | kk) != 0);
+            mma_bf16_ss_pair(d, ad, bd, idesc, (kb != w.kb0 || kk != 0) ? 1u : 0u);
           }
           mma_commit_pair(&empty[stage], 0x3);  // frees this stage in both CTAs
           if (++stage == kPairStages) {
@@ -348,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             phase ^= 1;
           }
         }
-        if (num_k > 0) {
+        if (w.kb1 > w.kb0) {
           mma_commit_pair(&tfull[acc], 0x3);
         } else {
           mbar_arrive_cluster(&tfull[acc], 0);
@@ -364,12 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      int mb, nb;
-      tile_of(t, num_m, num_n, mb, nb);
+      const WorkItem w = work_of(t, num_m, num_n, S, num_k);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      TileInfo ti{mb * kPairBM + 128 * static_cast<int>(rank), nb * BN, nb, M, N, q * 32 + lane, num_k == 0};
+      TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
+                  w.kb1 == w.kb0, w.s};
       Epi::apply(ep, taddr, ti);
       tc_fence_before();
       __syncwarp();

@@ -39,12 +39,16 @@ struct EpiLse {
     float* part_s;        // [n_tiles][ld]
     int64_t ld;
     float* zt;            // [N_v] target logit (single writer: the owning tile)
+    int32_t row_off;      // compacted row of GEMM row 0 (row chunk of the fused path)
+    float* z;             // fused path: fp32 logit chunk [rows][ldz] (cols >= n_cols: -inf), or null
+    int64_t ldz;
   };
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
-    const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;  // tile-relative target column
+    const int yl = valid ? (p.yc[p.row_off + r] - p.label_off - t.n0) : -1;  // tile-relative target column
     float m = -INFINITY, s = 0.f, zt = 0.f;
+    float4* zrow = (p.z && valid) ? reinterpret_cast<float4*>(p.z + static_cast<int64_t>(r) * p.ldz + t.n0) : nullptr;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float x[32];
@@ -54,6 +58,10 @@ struct EpiLse {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (cb + j >= p.n_cols) x[j] = -INFINITY;
+      }
+      if (zrow) {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) zrow[c * 8 + v] = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
       }
       if ((yl >> 5) == c) {
         const int jt = yl & 31;
@@ -82,7 +90,7 @@ struct EpiLse {
     if (valid) {
       p.part_m[t.n_blk * p.ld + r] = m;
       p.part_s[t.n_blk * p.ld + r] = s;
-      if (yl >= 0 && yl < BN && t.n0 + yl < p.n_cols) p.zt[r] = zt;
+      if (yl >= 0 && yl < BN && t.n0 + yl < p.n_cols) p.zt[p.row_off + r] = zt;
     }
   }
 };
@@ -142,14 +150,35 @@ struct EpiDH {
     const Header* hdr;     // c
     uint16_t* dhidden;     // [N][D] bf16
     const int32_t* idx;    // compact row -> token row
+    int32_t row_off;       // compacted row of GEMM row 0
+    int32_t use_c;         // 1: scale by c on output; 0: c already folded into G
+    float* part;           // split-K: fp32 partial slabs [ksplit][rows][ld] (reduced by reduce_dh_kernel)
+    int64_t part_stride;   // elements per slab
   };
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
-    const float cs = p.last_direct ? p.hdr->c : 1.f;
-    float* accrow = p.acc_buf + static_cast<int64_t>(r) * p.ld;
+    if (p.part) {  // split-K partial: plain fp32 store, no read-modify-write
+      float* prow = p.part + t.split * p.part_stride + static_cast<int64_t>(r) * p.ld;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float x[32];
+        load_chunk(taddr, c, t.zero_acc, x);
+        const int cb = t.n0 + c * 32;
+        if (!valid) continue;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const int col = cb + 4 * v;
+          if (col >= t.N) break;
+          *reinterpret_cast<float4*>(prow + col) = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+        }
+      }
+      return;
+    }
+    const float cs = (p.last_direct && p.use_c) ? p.hdr->c : 1.f;
+    float* accrow = p.acc_buf + static_cast<int64_t>(p.row_off + r) * p.ld;
     uint16_t* orow = nullptr;
-    if (valid && p.last_direct) orow = p.dhidden + static_cast<int64_t>(p.idx[r]) * p.ld;
+    if (valid && p.last_direct) orow = p.dhidden + static_cast<int64_t>(p.idx[p.row_off + r]) * p.ld;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float x[32];
@@ -187,11 +216,13 @@ struct EpiDW {
     int64_t ld;           // D
     int32_t accumulate;
     const Header* hdr;
+    int32_t use_c;        // 1: scale by c; 0: c already folded into G
   };
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    if (t.zero_acc && p.accumulate) return;  // K == 0 adds nothing (uniform across the CTA)
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
-    const float cs = p.hdr->c;
+    const float cs = p.use_c ? p.hdr->c : 1.f;
     float* row = p.dW + static_cast<int64_t>(r) * p.ld;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
@@ -212,6 +243,64 @@ struct EpiDW {
           a.w += o.w;
         }
         *reinterpret_cast<float4*>(row + col) = a;
+      }
+    }
+  }
+};
+
+// ============================================================ NEXT-2: AdamW in the dW epilogue
+// Optimizer-in-backward for the LM head (Sec. 4.1): a dW row block
+// is final when its tile leaves TMEM (the V-chunked backward writes each dW row
+// exactly once), so the epilogue applies the AdamW step there and no dW buffer
+// exists.  torch.optim.AdamW order: theta *= 1 - lr wd;
+// m = b1 m + (1 - b1) g; v = b2 v + (1 - b2) g^2;
+// theta -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps); W = bf16(theta).
+struct EpiAdamW {
+  struct Params {
+    float* theta;         // fp32 master weights, chunk row 0
+    float* exp_avg;
+    float* exp_avg_sq;
+    uint16_t* w;          // bf16 weights used by the GEMMs, rewritten
+    int64_t ld;           // D
+    const Header* hdr;    // c
+    float lr, beta1, beta2, eps, decay;  // decay = 1 - lr * weight_decay
+    float step_size, inv_sqrt_bc2;       // lr / bc1, 1 / sqrt(bc2)
+  };
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    const bool valid = r < t.M;
+    const float cs = p.hdr->c;
+    const int64_t rowoff = static_cast<int64_t>(r) * p.ld;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      float x[32];
+      load_chunk(taddr, c, t.zero_acc, x);
+      const int cb = t.n0 + c * 32;
+      if (!valid) continue;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int col = cb + 4 * v;
+        if (col >= t.N) break;
+        float4 th = *reinterpret_cast<const float4*>(p.theta + rowoff + col);
+        float4 m = *reinterpret_cast<const float4*>(p.exp_avg + rowoff + col);
+        float4 s = *reinterpret_cast<const float4*>(p.exp_avg_sq + rowoff + col);
+        float* thv = &th.x;
+        float* mv = &m.x;
+        float* sv = &s.x;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float g = cs * x[4 * v + e];
+          thv[e] = thv[e] * p.decay;
+          mv[e] = p.beta1 * mv[e] + (1.f - p.beta1) * g;
+          sv[e] = p.beta2 * sv[e] + (1.f - p.beta2) * g * g;
+          const float denom = __fsqrt_rn(sv[e]) * p.inv_sqrt_bc2 + p.eps;
+          thv[e] = thv[e] - p.step_size * __fdiv_rn(mv[e], denom);
+        }
+        *reinterpret_cast<float4*>(p.theta + rowoff + col) = th;
+        *reinterpret_cast<float4*>(p.exp_avg + rowoff + col) = m;
+        *reinterpret_cast<float4*>(p.exp_avg_sq + rowoff + col) = s;
+        *reinterpret_cast<uint2*>(p.w + rowoff + col) =
+            make_uint2(pack_bf16x2(th.x, th.y), pack_bf16x2(th.z, th.w));
       }
     }
   }
@@ -476,6 +565,118 @@ __global__ void __launch_bounds__(256) finalize_dh_kernel(const float* __restric
   for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
     const float4 a = src[v];
     dst[v] = make_uint2(pack_bf16x2(c * a.x, c * a.y), pack_bf16x2(c * a.z, c * a.w));
+  }
+}
+
+// ============================================================ fused fwd+bwd (row chunks)
+// S3 for one row chunk: partials [n_tiles][ld] of chunk rows m < M (M =
+// clamp(N_v - row_off, 0, cap)) -> lse, token loss (scattered to the token
+// rows) and the compact-row copies lse_c / ltok used by the next kernels.
+__global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restrict__ pm, const float* __restrict__ ps,
+                                                           int n_tiles, int64_t ld, int row_off, int cap,
+                                                           const float* __restrict__ zt,
+                                                           const int32_t* __restrict__ idx, const Header* hdr,
+                                                           float* __restrict__ lse_out, float* __restrict__ tok_out,
+                                                           float* __restrict__ lse_c, float* __restrict__ ltok) {
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= M) return;
+  float Mx = -INFINITY, S = 0.f;
+  for (int t = 0; t < n_tiles; ++t) Mx = fmaxf(Mx, pm[t * ld + m]);
+  for (int t = 0; t < n_tiles; ++t) S += ps[t * ld + m] * expf(pm[t * ld + m] - Mx);
+  const int r = row_off + m;
+  const float lse = Mx + logf(S);
+  const float l = lse - zt[r];
+  const int i = idx[r];
+  lse_out[i] = lse;
+  if (tok_out) tok_out[i] = l;
+  lse_c[r] = lse;
+  ltok[r] = l;
+}
+
+// S4 of the fused path without the recompute: the chunk's fp32 logits Z (kept
+// from the forward GEMM) -> G = s_i (exp(z - lse_i) - [j == y_i]) in bf16,
+// s_i = c (MEAN / SUM) or g_i (NONE); rows in [M, ceil64(M)) and columns
+// >= n_cols are zero.  One CTA per row, 8 columns per thread per step.
+__global__ void __launch_bounds__(256) fixup_g_kernel(const float* __restrict__ Z, int64_t ldz, int n_cols,
+                                                      int row_off, int cap, const int32_t* __restrict__ yc,
+                                                      int32_t label_off, const float* __restrict__ lse_c,
+                                                      const float* __restrict__ row_scale, const Header* hdr,
+                                                      uint16_t* __restrict__ G) {
+  const int m = blockIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= ((M + 63) & ~63)) return;
+  uint4* grow = reinterpret_cast<uint4*>(G + static_cast<int64_t>(m) * ldz);
+  const int nvec = static_cast<int>(ldz / 8);
+  if (m >= M) {
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) grow[v] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const int r = row_off + m;
+  const float lsel = lse_c[r] * kLog2e;
+  const int yl = yc[r] - label_off;
+  const float sc = hdr->c * (row_scale ? row_scale[r] : 1.f);
+  const float4* zrow = reinterpret_cast<const float4*>(Z + static_cast<int64_t>(m) * ldz);
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const float4 a = zrow[2 * v], b = zrow[2 * v + 1];
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const int c0 = 8 * v + j;
+      float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c0 == yl ? 1.f : 0.f);
+      float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c0 + 1 == yl ? 1.f : 0.f);
+      g0 = c0 < n_cols ? g0 * sc : 0.f;
+      g1 = c0 + 1 < n_cols ? g1 * sc : 0.f;
+      w[j / 2] = pack_bf16x2(g0, g1);
+    }
+    grow[v] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Split-K dH of a row chunk: dhidden[idx[row_off + m]] = bf16(sum_s part[s][m])
+// (c already folded into G), fixed split order.  One CTA per row.
+__global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict__ part, int ksplit,
+                                                        int64_t part_stride, int64_t D, int row_off, int cap,
+                                                        const int32_t* __restrict__ idx, const Header* hdr,
+                                                        uint16_t* __restrict__ dhidden) {
+  const int m = blockIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= M) return;
+  uint2* dst = reinterpret_cast<uint2*>(dhidden + static_cast<int64_t>(idx[row_off + m]) * D);
+  for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
+    float4 a = reinterpret_cast<const float4*>(part + static_cast<int64_t>(m) * D)[v];
+    for (int s = 1; s < ksplit; ++s) {
+      const float4 b = reinterpret_cast<const float4*>(part + s * part_stride + static_cast<int64_t>(m) * D)[v];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    dst[v] = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+  }
+}
+
+// Final S3 loss of the fused path: fixed-order sum of ltok[0, N_v) in fp64.
+__global__ void __launch_bounds__(1024) loss_reduce_kernel(const float* __restrict__ ltok, const Header* hdr,
+                                                           float* __restrict__ loss, int32_t* __restrict__ n_valid_out,
+                                                           int reduction) {
+  __shared__ double red[1024];
+  const int nv = hdr->n_valid;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nv; i += 1024) acc += ltok[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 512; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double L = red[0];
+    if (reduction == 0) L = nv > 0 ? L / nv : 0.0;
+    if (hdr->status & kStatusBadLabel) L = __longlong_as_double(0x7ff8000000000000ULL);
+    *loss = static_cast<float>(L);
+    if (n_valid_out) *n_valid_out = nv;
   }
 }
 

@@ -91,6 +91,78 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   return true;
 }
 
+// Fused fwd+bwd (lce_forward_backward): row chunks of Nc compacted tokens keep
+// their fp32 logits Z [Nc, ldv] and bf16 G [Nc, ldv]; 6 bytes per element are
+// bounded by the budget (default 4 GiB), never N x V_l.
+constexpr int64_t kDefaultFusedBudget = 4ll << 30;
+
+struct FusedPlan {
+  int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
+  size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, total;
+};
+
+bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
+  Plan base;
+  if (!make_plan(p, &base)) return false;
+  FusedPlan q{};
+  q.N = base.N;
+  q.D = base.D;
+  q.Vl = base.Vl;
+  q.cap = base.cap;
+  q.ldv = round_up(q.Vl, BN);
+  q.n_tiles = ceil_div(q.Vl, BN);
+  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
+  int64_t nc_max = (budget / (6 * q.ldv)) / kPairBM * kPairBM;
+  if (nc_max < kPairBM) nc_max = kPairBM;
+  if (nc_max > q.cap) nc_max = q.cap;
+  q.n_chunks = ceil_div(q.cap, nc_max);
+  q.Nc = round_up(ceil_div(q.cap, q.n_chunks), kPairBM);  // balanced chunks
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = static_cast<size_t>(round_up(static_cast<int64_t>(off + bytes), 1024));
+    return o;
+  };
+  q.hdr = take(sizeof(Header));
+  q.idx = take(q.cap * 4);
+  q.yc = take(q.cap * 4);
+  q.zt = take(q.cap * 4);
+  q.lsec = take(q.cap * 4);
+  q.gsc = take(q.cap * 4);
+  q.ltok = take(q.cap * 4);
+  q.hc = take(static_cast<size_t>((q.n_chunks * q.Nc) * q.D * 2));
+  q.pm = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
+  q.ps = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
+  q.z = take(static_cast<size_t>(q.Nc * q.ldv * 4));
+  q.g = take(static_cast<size_t>(q.Nc * q.ldv * 2));
+  q.total = off;
+  *fp = q;
+  return true;
+}
+
+bool use_pair();
+
+// Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
+// work items fill the persistent grid's last wave to >= 97% (else the best),
+// with the fp32 slabs fitting in the logit chunk buffer (split * D <= ldv).
+int dh_split(const FusedPlan& fp, int sms) {
+  const int64_t units = use_pair() ? sms / 2 : sms;
+  const int64_t rows = use_pair() ? 256 : 128;
+  const int64_t tiles = ceil_div(fp.Nc, rows) * ceil_div(fp.D, BN);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 8 && s * fp.D <= fp.ldv; ++s) {
+    const int64_t items = tiles * s;
+    const double eff = static_cast<double>(items) / (ceil_div(items, units) * units);
+    if (eff > best_eff + 1e-9) {
+      best = s;
+      best_eff = eff;
+    }
+    if (eff >= 0.97) break;
+  }
+  return best;
+}
+
 // ------------------------------------------------------------------ device / driver
 typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -139,6 +211,7 @@ lce_status_t device_info(DevInfo* out) {
     LCE_SMEM_ATTR(false, false, EpiG);
     LCE_SMEM_ATTR(false, true, EpiDH);
     LCE_SMEM_ATTR(true, true, EpiDW);
+    LCE_SMEM_ATTR(true, true, EpiAdamW);
     LCE_SMEM_ATTR(false, false, EpiStore);
     LCE_SMEM_ATTR(false, true, EpiStore);
     LCE_SMEM_ATTR(true, false, EpiStore);
@@ -423,7 +496,7 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
   LCE_TRY(map_kmajor(&ta, hc, pl.cap, pl.D, pl.D, BM));
   LCE_TRY(map_kmajor(&tb, weight, pl.Vl, pl.D, pl.D, b_box_rows()));
   GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(pl.Vl)};
-  EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), static_cast<int32_t>(pl.Vl), pm, ps, pl.cap, zt};
+  EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), static_cast<int32_t>(pl.Vl), pm, ps, pl.cap, zt, 0, nullptr, 0};
   LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s)));
 
   const unsigned cblocks = static_cast<unsigned>(pl.nblocks);
@@ -461,13 +534,26 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
   return LCE_OK;
 }
 
-lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
-                          const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
-                          float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
-                          void* stream) {
+}  // extern "C"
+
+namespace {
+
+// In-backward AdamW state for lce_backward_adamw (NEXT-2); null for lce_backward.
+struct AdamArgs {
+  float* theta;
+  float* exp_avg;
+  float* exp_avg_sq;
+  uint16_t* w;
+  lce_adamw_t hp;
+};
+
+lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+                           const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
+                           float* dweight, int accumulate_dweight, const AdamArgs* adam, void* workspace,
+                           size_t workspace_bytes, void* stream) {
   Plan pl;
   LCE_TRY(validate(p, comm, workspace_bytes, workspace, &pl));
-  if (!weight || !dweight) return LCE_ERR_NULL;
+  if (!weight || (!dweight && !adam)) return LCE_ERR_NULL;
   if (pl.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
   const void* ptrs[] = {hidden, weight, labels, lse, grad_loss, dhidden, dweight};
   for (const void* q : ptrs)
@@ -478,9 +564,22 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Header* hdr = reinterpret_cast<Header*>(ws + pl.hdr);
 
-  if (pl.N == 0) {
+  if (pl.N == 0 && !adam) {
     if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, pl.Vl * pl.D * sizeof(float), s));
     return LCE_OK;
+  }
+  if (pl.N == 0) {  // empty batch, in-backward AdamW: the step still runs with g = 0
+    LCE_CUDA(cudaMemsetAsync(hdr, 0, sizeof(Header), s));
+    CUtensorMap t_any;
+    LCE_TRY(map_mnmajor(&t_any, weight, pl.Vl, pl.D, pl.D));
+    const lce_adamw_t& h = adam->hp;
+    const double bc1 = 1.0 - pow(static_cast<double>(h.beta1), static_cast<double>(h.step));
+    const double bc2 = 1.0 - pow(static_cast<double>(h.beta2), static_cast<double>(h.step));
+    GemmDims d{nullptr, static_cast<int32_t>(pl.Vl), nullptr, 0, static_cast<int32_t>(pl.D)};
+    EpiAdamW::Params ep{adam->theta, adam->exp_avg, adam->exp_avg_sq, adam->w, pl.D, hdr, h.lr, h.beta1, h.beta2,
+                        h.eps, 1.f - h.lr * h.weight_decay, static_cast<float>(h.lr / bc1),
+                        static_cast<float>(1.0 / sqrt(bc2))};
+    return launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_any, t_any, d, ep, dev.sms, s);
   }
   const int N = static_cast<int>(pl.N);
   int32_t* idx = reinterpret_cast<int32_t*>(ws + pl.idx);
@@ -530,7 +629,7 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
     // S6: dH (+)= G_c W_c   (A = G_c K-major over vocab, B = W_c MN-major)
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
-      EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx};
+      EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx, 0, 1};
       LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
     }
     // S7 (vocab-parallel): once the last chunk's dH partial is complete, its
@@ -545,8 +644,19 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
     // S5: dW_c = c G_c^T H   (A = G_c MN-major, B = H_c MN-major, K = N_v)
     {
       GemmDims d{nullptr, static_cast<int32_t>(vc), &hdr->n_valid, 0, static_cast<int32_t>(pl.D)};
-      EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr};
-      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+      if (!adam) {
+        EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
+        LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+      } else {  // NEXT-2: the AdamW step of these W rows happens in the dW epilogue
+        const lce_adamw_t& h = adam->hp;
+        const double bc1 = 1.0 - pow(static_cast<double>(h.beta1), static_cast<double>(h.step));
+        const double bc2 = 1.0 - pow(static_cast<double>(h.beta2), static_cast<double>(h.step));
+        const int64_t o = v0 * pl.D;
+        EpiAdamW::Params ep{adam->theta + o, adam->exp_avg + o, adam->exp_avg_sq + o, adam->w + o, pl.D, hdr,
+                            h.lr, h.beta1, h.beta2, h.eps, 1.f - h.lr * h.weight_decay,
+                            static_cast<float>(h.lr / bc1), static_cast<float>(1.0 / sqrt(bc2))};
+        LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+      }
     }
   }
   if (multi) {
@@ -554,6 +664,154 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
     LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
     LaunchScope sc(LCE_K_FINAL, s);
     finalize_dh_kernel<<<static_cast<unsigned>(pl.N), 256, 0, s>>>(dh, pl.D, idx, hdr, dhidden);
+    LCE_TRY(last_error());
+  }
+  return LCE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+                          const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
+                          float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return backward_impl(p, comm, hidden, weight, labels, lse, grad_loss, dhidden, dweight, accumulate_dweight, nullptr,
+                       workspace, workspace_bytes, stream);
+}
+
+lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, uint16_t* weight,
+                                const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
+                                float* master_weight, float* exp_avg, float* exp_avg_sq, const lce_adamw_t* hp,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  if (!hp || !master_weight || !exp_avg || !exp_avg_sq || !weight) return LCE_ERR_NULL;
+  if (hp->step < 1 || !(hp->beta1 >= 0.f && hp->beta1 < 1.f) || !(hp->beta2 >= 0.f && hp->beta2 < 1.f) ||
+      !(hp->eps > 0.f) || !(hp->lr >= 0.f) || !(hp->weight_decay >= 0.f))
+    return LCE_ERR_SHAPE;
+  if (!aligned16(master_weight) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) return LCE_ERR_ALIGN;
+  AdamArgs a{master_weight, exp_avg, exp_avg_sq, weight, *hp};
+  return backward_impl(p, comm, hidden, weight, labels, lse, grad_loss, dhidden, nullptr, 0, &a, workspace,
+                       workspace_bytes, stream);
+}
+
+size_t lce_fused_workspace_bytes(const lce_problem_t* p) {
+  FusedPlan fp;
+  if (!make_fused_plan(p, &fp)) return 0;
+  return fp.total;
+}
+
+lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden,
+                                  const uint16_t* weight, const int32_t* labels, const float* grad_loss,
+                                  float* loss, float* lse, float* token_loss, int32_t* n_valid, uint16_t* dhidden,
+                                  float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
+                                  void* stream) {
+  if (!p) return LCE_ERR_NULL;
+  if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
+  FusedPlan fp;
+  if (!make_fused_plan(p, &fp)) return LCE_ERR_SHAPE;
+  if (comm) return LCE_ERR_COMM;  // vocab-parallel runs through lce_forward + lce_backward
+  if (p->vocab_start != 0 || p->vocab_local != p->vocab_total) return LCE_ERR_COMM;
+  if (!workspace || !weight || !loss || !dweight) return LCE_ERR_NULL;
+  if (fp.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
+  const void* ptrs[] = {hidden, weight, labels, grad_loss, loss, lse, token_loss, n_valid, dhidden, dweight, workspace};
+  for (const void* q : ptrs)
+    if (q && !aligned16(q)) return LCE_ERR_ALIGN;
+  if (workspace_bytes < fp.total) return LCE_ERR_WORKSPACE;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
+  if (fp.N == 0) {
+    LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
+    if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
+    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, fp.Vl * fp.D * sizeof(float), s));
+    return LCE_OK;
+  }
+  const int N = static_cast<int>(fp.N);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + fp.idx);
+  int32_t* yc = reinterpret_cast<int32_t*>(ws + fp.yc);
+  float* zt = reinterpret_cast<float*>(ws + fp.zt);
+  float* lsec = reinterpret_cast<float*>(ws + fp.lsec);
+  float* gsc = reinterpret_cast<float*>(ws + fp.gsc);
+  float* ltok = reinterpret_cast<float*>(ws + fp.ltok);
+  uint16_t* hc = reinterpret_cast<uint16_t*>(ws + fp.hc);
+  float* pm = reinterpret_cast<float*>(ws + fp.pm);
+  float* ps = reinterpret_cast<float*>(ws + fp.ps);
+  float* Z = reinterpret_cast<float*>(ws + fp.z);
+  uint16_t* G = reinterpret_cast<uint16_t*>(ws + fp.g);
+  const float* row_grad = p->reduction == LCE_NONE ? grad_loss : nullptr;
+
+  {
+    LaunchScope sc(LCE_K_PREP, s);
+    prep_kernel<<<1, 1024, 0, s>>>(labels, N, p->ignore_index, p->vocab_total, idx, yc, zt, lse, token_loss, hdr,
+                                   grad_loss, p->reduction);
+    LCE_TRY(last_error());
+  }
+  {
+    LaunchScope sc(LCE_K_GATHER, s);
+    gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden, fp.D, N, idx, hdr, hc, nullptr, nullptr,
+                                                               row_grad, gsc, labels, p->ignore_index,
+                                                               p->vocab_total, dhidden);
+    LCE_TRY(last_error());
+  }
+  const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
+  CUtensorMap t_w_k, t_w_mn, t_g_k, t_g_mn;
+  LCE_TRY(map_kmajor(&t_w_k, weight, fp.Vl, fp.D, fp.D, b_box_rows()));
+  LCE_TRY(map_mnmajor(&t_w_mn, weight, fp.Vl, fp.D, fp.D));
+  LCE_TRY(map_kmajor(&t_g_k, G, fp.Nc, fp.ldv, fp.ldv, BM));
+  LCE_TRY(map_mnmajor(&t_g_mn, G, fp.Nc, fp.ldv, fp.ldv));
+  for (int64_t q = 0; q < fp.n_chunks; ++q) {
+    const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
+    const uint16_t* hq = hc + static_cast<int64_t>(r0) * fp.D;
+    CUtensorMap t_h_k, t_h_mn;
+    LCE_TRY(map_kmajor(&t_h_k, hq, fp.Nc, fp.D, fp.D, BM));
+    LCE_TRY(map_mnmajor(&t_h_mn, hq, fp.Nc, fp.D, fp.D));
+    // S1+S2 (+ keep the fp32 logit chunk): z = H_q W^T, online LSE partials
+    {
+      GemmDims d{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
+      EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, Z, fp.ldv};
+      LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
+    }
+    {  // S3 for the chunk rows
+      LaunchScope sc(LCE_K_COMBINE, s);
+      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
+          pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse, token_loss, lsec, ltok);
+      LCE_TRY(last_error());
+    }
+    {  // S4 without recompute: G = s_i (softmax - onehot) from the kept logits
+      LaunchScope sc(LCE_K_BWD_G, s);
+      fixup_g_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, fp.ldv, Vl, r0, Nc, yc,
+                                                                  static_cast<int32_t>(p->vocab_start), lsec,
+                                                                  row_grad ? gsc : nullptr, hdr, G);
+      LCE_TRY(last_error());
+    }
+    // S6: dH rows of the chunk = G_q W (K = V_l).  Only ceil(Nc/256) x ceil(D/256)
+    // output tiles with a very long K: split K so the persistent grid sees whole
+    // waves; fp32 partial slabs reuse the (now dead) logit chunk Z.
+    {
+      const int split = dh_split(fp, dev.sms);
+      GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
+      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, split > 1 ? Z : nullptr, fp.Nc * fp.D};
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
+      if (split > 1) {
+        LaunchScope sc(LCE_K_FINAL, s);
+        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+                                                                     dhidden);
+        LCE_TRY(last_error());
+      }
+    }
+    // S5: dW (+)= G_q^T H_q (K = chunk rows)
+    {
+      GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
+      EpiDW::Params ep{dweight, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
+      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, dev.sms, s)));
+    }
+  }
+  {
+    LaunchScope sc(LCE_K_COMBINE, s);
+    loss_reduce_kernel<<<1, 1024, 0, s>>>(ltok, hdr, loss, n_valid, p->reduction);
     LCE_TRY(last_error());
   }
   return LCE_OK;

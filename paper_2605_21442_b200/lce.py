@@ -13,7 +13,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import KERNEL_CLASSES, LCE_K_COUNT, Problem, check, lib
+from ._lib import KERNEL_CLASSES, LCE_K_COUNT, AdamW, Problem, check, lib
 from .dist import broadcast_bytes, shard_range  # noqa: F401
 
 MEAN, SUM, NONE = 0, 1, 2
@@ -171,6 +171,86 @@ def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, l
                            _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(dweight),
                            1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)), "lce_backward")
     return dhidden, dweight
+
+
+def backward_adamw(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, lse: torch.Tensor,
+                   master_weight: torch.Tensor, exp_avg: torch.Tensor, exp_avg_sq: torch.Tensor, *, lr: float,
+                   step: int, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.0,
+                   grad_loss: Optional[torch.Tensor] = None, ignore_index: int = -100, reduction: str = "mean",
+                   comm: Optional[Comm] = None, vocab_start: int = 0, vocab_total: Optional[int] = None,
+                   dhidden: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+                   chunk_budget_bytes: int = 0, stream=None) -> torch.Tensor:
+    """lce_backward with the LM-head AdamW step fused into the dW epilogue
+    (optimizer-in-backward).  Updates weight (bf16), master_weight,
+    exp_avg, exp_avg_sq in place; returns dhidden."""
+    _check_inputs(hidden, weight, labels)
+    for t in (master_weight, exp_avg, exp_avg_sq):
+        if t.dtype != torch.float32 or t.shape != weight.shape or not t.is_contiguous():
+            raise ValueError("master_weight / exp_avg / exp_avg_sq must be contiguous fp32 like weight")
+    N, D = hidden.shape
+    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
+    dev = hidden.device
+    ws = _ws_for(workspace, prob, dev)
+    if dhidden is None:
+        dhidden = torch.empty_like(hidden)
+    if grad_loss is not None:
+        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+    hp = AdamW(lr, betas[0], betas[1], eps, weight_decay, step)
+    check(lib.lce_backward_adamw(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
+                                 _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(master_weight),
+                                 _ptr(exp_avg), _ptr(exp_avg_sq), ctypes.byref(hp), _ptr(ws), ws.numel(),
+                                 _stream(stream)), "lce_backward_adamw")
+    return dhidden
+
+
+def fused_workspace_bytes(problem: Problem) -> int:
+    return int(lib.lce_fused_workspace_bytes(ctypes.byref(problem)))
+
+
+def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *,
+                     grad_loss: Optional[torch.Tensor] = None, ignore_index: int = -100, reduction: str = "mean",
+                     with_token_loss: bool = False, dhidden: Optional[torch.Tensor] = None,
+                     dweight: Optional[torch.Tensor] = None, accumulate_dweight: bool = False,
+                     workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0, stream=None,
+                     out: Optional[dict] = None) -> dict:
+    """Fused forward + backward without logit recompute (lce_forward_backward).
+
+    Returns {loss, lse, n_valid, token_loss, dhidden, dweight}."""
+    _check_inputs(hidden, weight, labels)
+    N, D = hidden.shape
+    prob = make_problem(N, D, weight.shape[0], ignore_index=ignore_index, reduction=reduction,
+                        chunk_budget_bytes=chunk_budget_bytes)
+    dev = hidden.device
+    need = fused_workspace_bytes(prob)
+    if need == 0:
+        raise ValueError("invalid LCE problem shape")
+    if workspace is None:
+        workspace = _default_ws.setdefault(str(dev) + ":fused", Workspace())
+    ws = workspace.get(need, dev)
+    with_token_loss = with_token_loss or reduction == "none"
+    if out is None:
+        out = {
+            "loss": torch.empty(1, dtype=torch.float32, device=dev),
+            "lse": torch.empty(N, dtype=torch.float32, device=dev),
+            "n_valid": torch.empty(1, dtype=torch.int32, device=dev),
+            "token_loss": torch.empty(N, dtype=torch.float32, device=dev) if with_token_loss else None,
+        }
+    if dhidden is None:
+        dhidden = torch.empty_like(hidden)
+    if dweight is None:
+        dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
+    if grad_loss is not None:
+        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+        if grad_loss.numel() != (N if reduction == "none" else 1):
+            raise ValueError("grad_loss must have N elements for 'none' and 1 otherwise")
+    check(lib.lce_forward_backward(ctypes.byref(prob), None, _ptr(hidden), _ptr(weight), _ptr(labels),
+                                   _ptr(grad_loss), _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["token_loss"]),
+                                   _ptr(out["n_valid"]), _ptr(dhidden), _ptr(dweight),
+                                   1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)),
+          "lce_forward_backward")
+    out["dhidden"], out["dweight"] = dhidden, dweight
+    return out
 
 
 def check_device_status(workspace: Optional[Workspace] = None, device=None, stream=None) -> None:

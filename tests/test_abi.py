@@ -15,9 +15,9 @@ HEADER = os.path.join(ROOT, "include", "lce.h")
 
 @pytest.fixture(scope="module")
 def L():
-    from paper_2605_21442_b200 import build
+    from __graft_entry__ import load_build_module
 
-    build.build()
+    load_build_module().build()
     from paper_2605_21442_b200 import _lib
 
     return _lib

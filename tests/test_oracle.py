@@ -395,3 +395,38 @@ def test_none_with_uniform_weights_is_mean():
     bm = lce_backward(H, W, y, reduction="mean")
     np.testing.assert_allclose(bn["dH"], bm["dH"], rtol=1e-13, atol=1e-17)
     np.testing.assert_allclose(bn["dW"], bm["dW"], rtol=1e-13, atol=1e-17)
+
+
+# ---------------------------------------------------------------- AdamW (Sec. 4.1)
+def test_adamw_spec_examples():
+    """S:357 decay-only step (g = 0, wd = 0.01, lr = 2e-5 from App. D) and the
+    scalar first step theta = g = 1, betas (0.9, 0.999), wd = 0, hand-derived:
+    m = 0.1, v = 0.001, m_hat = v_hat = 1 -> theta' = 1 - lr / (1 + eps)."""
+    from oracle import adamw_step
+
+    th, m, v = adamw_step(np.array([3.0, -1.5]), np.zeros(2), np.zeros(2), np.zeros(2), step=1, lr=2e-5,
+                          weight_decay=0.01)
+    np.testing.assert_allclose(th, np.array([3.0, -1.5]) * (1 - 2e-7), rtol=1e-15)
+    assert not m.any() and not v.any()
+    th, m, v = adamw_step(np.array([1.0]), np.array([1.0]), np.zeros(1), np.zeros(1), step=1, lr=1e-3)
+    assert m[0] == pytest.approx(0.1, rel=1e-15) and v[0] == pytest.approx(0.001, rel=1e-12)
+    assert th[0] == pytest.approx(1 - 1e-3 / (1 + 1e-8), rel=1e-14)
+
+
+def test_adamw_matches_torch_fp64_multi_step():
+    """P10-style library pin: torch.optim.AdamW (CPU, fp64) over 5 steps."""
+    from oracle import adamw_step
+
+    rng = np.random.default_rng(4)
+    th0 = rng.standard_normal((7, 5))
+    p = torch.nn.Parameter(torch.tensor(th0))
+    opt = torch.optim.AdamW([p], lr=3e-3, betas=(0.9, 0.95), eps=1e-6, weight_decay=0.1)
+    th, m, v = th0.copy(), np.zeros_like(th0), np.zeros_like(th0)
+    for t in range(1, 6):
+        g = rng.standard_normal((7, 5))
+        p.grad = torch.tensor(g)
+        opt.step()
+        th, m, v = adamw_step(th, g, m, v, t, lr=3e-3, beta1=0.9, beta2=0.95, eps=1e-6, weight_decay=0.1)
+    np.testing.assert_allclose(th, p.detach().numpy(), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(m, opt.state[p]["exp_avg"].numpy(), rtol=1e-13, atol=1e-16)
+    np.testing.assert_allclose(v, opt.state[p]["exp_avg_sq"].numpy(), rtol=1e-13, atol=1e-18)

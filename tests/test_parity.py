@@ -315,6 +315,156 @@ def test_autograd_none_reduction(cuda_lib):
     assert fro_rel(h.grad.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
 
 
+# ------------------------------------------------------------ fused fwd+bwd (no recompute)
+def fused_run(inp, reduction="mean", grad=None, budget=0, accumulate_into=None):
+    import paper_2605_21442_b200 as F
+
+    g = None
+    if grad is not None:
+        g = torch.as_tensor(grad, dtype=torch.float32, device=inp.hidden.device).reshape(-1)
+    dw0 = None if accumulate_into is None else accumulate_into.clone()
+    out = F.forward_backward(inp.hidden, inp.weight, inp.labels, grad_loss=g, ignore_index=inp.ignore_index,
+                             reduction=reduction, with_token_loss=True, chunk_budget_bytes=budget, dweight=dw0,
+                             accumulate_dweight=accumulate_into is not None)
+    torch.cuda.synchronize()
+    return {
+        "loss": out["loss"].item(), "n_valid": int(out["n_valid"].item()),
+        "lse": out["lse"].cpu().double().numpy(), "tok": out["token_loss"].cpu().double().numpy(),
+        "dH": out["dhidden"].float().cpu().double().numpy(), "dW": out["dweight"].cpu().double().numpy(),
+    }
+
+
+@pytest.mark.parametrize("reduction", ["mean", "sum"])
+@pytest.mark.parametrize("regime", ["random", "confident"])
+def test_fused_tiny_config(cuda_lib, variant, reduction, regime):
+    inp = make_config("tiny", device="cuda", regime=regime)
+    assert_parity(fused_run(inp, reduction), oracle_run(inp, reduction), inp.labels.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["llama8b", "qwen7b"])
+def test_fused_config_shapes_reduced_n(cuda_lib, name):
+    c = CONFIGS[name]
+    N = 300
+    labels = packed_labels(2048, c["V"], seed=0)[:N] if c["labels"] == "packed" else None
+    inp = make_inputs(N, c["D"], c["V"], k=c["k"], device="cuda", ignore_frac=0.1, label_override=labels,
+                      regime="confident")
+    assert_parity(fused_run(inp), oracle_run(inp), inp.labels.cpu().numpy())
+
+
+@pytest.mark.parametrize("N,D,V", [(1, 64, 1000), (129, 72, 256), (200, 8, 513), (260, 136, 2)])
+def test_fused_ragged_shapes(cuda_lib, N, D, V):
+    inp = small(N, D, V, seed=N + 1)
+    assert_parity(fused_run(inp), oracle_run(inp), inp.labels.cpu().numpy())
+
+
+def test_fused_many_row_chunks_with_packed_labels(cuda_lib, variant):
+    """Row chunks of 256 (tiny budget): several chunks, trailing chunks with no
+    valid row (packed labels compact to the front), dW accumulated across chunks."""
+    V, D = 3000, 128
+    lab = packed_labels(2048, V, seed=1)[:1100]
+    inp = small(1100, D, V, labels=lab)
+    budget = 256 * 6 * 3072  # Nc = 256 rows per chunk
+    g = fused_run(inp, budget=budget)
+    assert_parity(g, oracle_run(inp), lab)
+    one = fused_run(inp)
+    np.testing.assert_array_equal(g["lse"], one["lse"])
+    assert fro_rel(g["dW"], one["dW"]) <= 1e-5
+
+
+def test_fused_none_accumulate_and_empty(cuda_lib):
+    inp = small(300, 64, 1000, seed=11)
+    gvec = np.linspace(-2, 1, 300)
+    H, W, y = np_inputs(inp)
+    b = lce_backward(H, W, y, reduction="none", grad_loss=gvec)
+    f = lce_forward(H, W, y, reduction="none")
+    base = torch.randn(1000, 64, device="cuda")
+    g = fused_run(inp, "none", grad=gvec, accumulate_into=base)
+    assert np.abs(g["tok"] - f["token_loss"]).max() <= LSE_TOL * np.abs(f["lse"]).max()
+    assert fro_rel(g["dH"], b["dH"]) <= GRAD_TOL
+    assert fro_rel(g["dW"] - base.cpu().double().numpy(), b["dW"]) <= GRAD_TOL
+    e = fused_run(small(0, 64, 1000))
+    assert e["loss"] == 0 and e["n_valid"] == 0 and not e["dW"].any()
+    allign = fused_run(small(300, 64, 1000, labels=np.full(300, IGNORE, dtype=np.int32)))
+    assert allign["loss"] == 0 and not allign["dH"].any() and not allign["dW"].any()
+
+
+def test_fused_matches_recompute_path(cuda_lib):
+    """Same inputs through lce_forward + lce_backward and lce_forward_backward:
+    identical lse/loss (same forward GEMM), gradients within bf16 rounding."""
+    inp = small(700, 256, 5000, seed=12, regime="confident")
+    a, b = gpu_run(inp), fused_run(inp)
+    np.testing.assert_array_equal(a["lse"], b["lse"])
+    assert abs(a["loss"] - b["loss"]) <= 1e-6 * abs(a["loss"])
+    assert fro_rel(b["dH"], a["dH"]) <= 5e-3 and fro_rel(b["dW"], a["dW"]) <= 5e-3
+
+
+# ------------------------------------------------------------ NEXT-2: AdamW in the dW epilogue
+def _adam_state(V, D, seed):
+    g = torch.Generator().manual_seed(seed)
+    theta = torch.randn(V, D, generator=g) * 0.05
+    m = torch.randn(V, D, generator=g) * 1e-3
+    v = torch.rand(V, D, generator=g) * 1e-6 + 1e-7
+    return theta, m, v
+
+
+@pytest.mark.parametrize("N,D,V,budget", [(300, 64, 1000, 0), (300, 128, 3000, 300 * 2 * 512), (0, 64, 1000, 0)])
+def test_backward_adamw_matches_oracle_step(cuda_lib, variant, N, D, V, budget):
+    """P:137-160 optimizer-in-backward: the fused AdamW step on the LM head
+    equals the oracle's dW followed by the oracle's AdamW step."""
+    import paper_2605_21442_b200 as F
+    from oracle import adamw_step
+
+    inp = small(N, D, V, seed=13)
+    theta, m, v = _adam_state(V, D, 5)
+    hp = dict(lr=1e-3, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1, step=7)
+    w = theta.to(torch.bfloat16).cuda()
+    th_d, m_d, v_d = theta.cuda(), m.cuda(), v.cuda()
+    out = F.forward(inp.hidden, w, inp.labels)
+    F.backward_adamw(inp.hidden, w, inp.labels, out["lse"], th_d, m_d, v_d, chunk_budget_bytes=budget, **hp)
+    torch.cuda.synchronize()
+    H, _, y = np_inputs(inp)
+    Wb = w.float().cpu().numpy() if N == 0 else theta.to(torch.bfloat16).float().numpy()
+    gW = lce_backward(H, Wb, y)["dW"] if N > 0 else np.zeros((V, D))
+    th_o, m_o, v_o = adamw_step(theta.double().numpy(), gW, m.double().numpy(), v.double().numpy(), hp["step"],
+                                lr=hp["lr"], beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=0.1)
+    m0, v0 = m.double().numpy(), v.double().numpy()
+    # gradient contributions carry the GEMM's bf16-G error; the moments' old parts are exact
+    assert fro_rel(m_d.cpu().double().numpy() - 0.9 * m0, m_o - 0.9 * m0) <= GRAD_TOL
+    assert fro_rel(v_d.cpu().double().numpy() - 0.95 * v0, v_o - 0.95 * v0) <= 2 * GRAD_TOL
+    dth = th_d.cpu().double().numpy() - theta.double().numpy()
+    assert fro_rel(dth, th_o - theta.double().numpy()) <= GRAD_TOL
+    assert torch.equal(w.cpu(), th_d.cpu().to(torch.bfloat16))  # W = bf16(theta) (RNE)
+
+
+def test_backward_adamw_equals_dw_then_torch_adamw(cuda_lib):
+    """in-backward AdamW == standard AdamW applied to the same dW (K=1)."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(500, 256, 5000, seed=14)
+    theta, m, v = _adam_state(5000, 256, 6)
+    w = theta.to(torch.bfloat16).cuda()
+    out = F.forward(inp.hidden, w, inp.labels)
+    _, dW = F.backward(inp.hidden, w, inp.labels, out["lse"])
+    p = torch.nn.Parameter(theta.clone().cuda())
+    opt = torch.optim.AdamW([p], lr=2e-4, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, foreach=False)
+    p.grad = torch.zeros_like(p)
+    opt.step()  # step 1 on a zero grad to reach step 2 with nonzero state
+    opt.state[p]["exp_avg"].copy_(m.cuda())
+    opt.state[p]["exp_avg_sq"].copy_(v.cuda())
+    p.data.copy_(theta.cuda())
+    p.grad = dW.clone()
+    opt.step()
+    th_d, m_d, v_d = theta.cuda(), m.cuda(), v.cuda()
+    F.backward_adamw(inp.hidden, w, inp.labels, out["lse"], th_d, m_d, v_d, lr=2e-4, betas=(0.9, 0.999), eps=1e-8,
+                     weight_decay=0.01, step=2)
+    torch.cuda.synchronize()
+    assert torch.allclose(m_d, opt.state[p]["exp_avg"], rtol=1e-5, atol=1e-12)
+    assert torch.allclose(v_d, opt.state[p]["exp_avg_sq"], rtol=1e-5, atol=1e-15)
+    dref = p.detach() - theta.cuda()
+    dgot = th_d - theta.cuda()
+    assert ((dgot - dref).abs() <= 1e-4 * dref.abs() + 1e-9).all()
+
+
 # ------------------------------------------------------------ full size, bench launch configuration
 @pytest.mark.parametrize("name", ["llama8b", "qwen7b"])
 def test_full_size_sampled_rows_and_invariants(cuda_lib, name):
