@@ -289,7 +289,7 @@ def main():
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.config, {}).get(dom)
+            traffic = json.load(open(tp)).get(args.config + ("_fused" if fused else ""), {}).get(dom)
         roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s", "frac": achieved / sus,
                 "traffic": traffic, "kernel": dom, "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                 "flops_per_launch": per_launch_flops,

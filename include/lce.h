@@ -176,6 +176,28 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
                                   int accumulate_dweight, void* workspace,
                                   size_t workspace_bytes, void* stream);
 
+/* ---- linear knowledge distillation (NEXT-4) ----------------
+ * Forward KL of a teacher head against a student head, both projected and
+ * reduced chunk by chunk like lce_forward_backward (neither N x V logit matrix
+ * exists):  l_i = -sum_j p_T(i,j) log p_S(i,j) = lse_S(i) - sum_j p_T(i,j) z_S(i,j)
+ * for rows with labels[i] != ignore_index (label values are only a mask),
+ * z_S = H_S W_S^T, z_T = H_T W_T^T, reductions as lce_problem_t.reduction.
+ * Student gradients dz_S = s_i (p_S - p_T):  dhidden_s = dz_S W_S (bf16),
+ * dweight_s = dz_S^T H_S (fp32, overwrite or accumulate); the teacher gets none.
+ *   p->hidden_dim = D_S, teacher_dim = D_T (% 8 == 0); hidden_s [N, D_S],
+ *   weight_s [V, D_S], hidden_t [N, D_T], weight_t [V, D_T] (bf16);
+ *   grad_loss / loss / token_loss / n_valid as lce_forward_backward.
+ * One GPU only (vocab_local == vocab_total). */
+size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim);
+lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim,
+                                     const uint16_t* hidden_s, const uint16_t* weight_s,
+                                     const uint16_t* hidden_t, const uint16_t* weight_t,
+                                     const int32_t* labels, const float* grad_loss,
+                                     float* loss, float* token_loss, int32_t* n_valid,
+                                     uint16_t* dhidden_s, float* dweight_s,
+                                     int accumulate_dweight, void* workspace,
+                                     size_t workspace_bytes, void* stream);
+
 /* Synchronises `stream`, reads the status word of `workspace` and returns
  * LCE_ERR_LABEL_RANGE if the most recent lce_forward / lce_backward that used
  * this workspace saw a bad label, LCE_OK otherwise.  Every call rewrites the

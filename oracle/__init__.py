@@ -16,4 +16,6 @@ from .lce_oracle import (  # noqa: F401
     shard_backward,
     combine_shard_stats,
     adamw_step,
+    kd_forward,
+    kd_backward,
 )

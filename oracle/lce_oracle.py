@@ -51,6 +51,8 @@ __all__ = [
     "shard_backward",
     "combine_shard_stats",
     "adamw_step",
+    "kd_forward",
+    "kd_backward",
 ]
 
 
@@ -246,6 +248,68 @@ def shard_backward(hidden, weight_shard, labels, vocab_start: int, lse, c: float
         dH[rows] = G @ Wr
         dW = G.T @ H[rows]
     return {"dH_partial": dH, "dW_shard": dW}
+
+
+def kd_forward(hidden_s, weight_s, hidden_t, weight_t, labels, ignore_index: int = IGNORE_INDEX,
+               reduction: str = "mean") -> dict:
+    """Linear knowledge-distillation loss (forward KL), fp64 -- NEXT-4.
+
+    P:35 (Fig. 1 objective box: "SFT CE / LCE / DPO / KD") and P:125-126
+    ("knowledge distillation with dedicated KD losses") name the objective but
+    give no formula.  Reading R23 (torchtune's forward-KL convention): for rows
+    with labels != ignore_index,
+        l_i = - sum_j p_T(i, j) log p_S(i, j) = lse_S(i) - sum_j p_T(i, j) z_S(i, j),
+    z_S = H_S W_S^T (student), z_T = H_T W_T^T (teacher), p = softmax; mean
+    over N_v or sum.  Label values are not used, only the ignore mask.
+    """
+    Hs, Ws, Ht, Wt = (_as_f64(a) for a in (hidden_s, weight_s, hidden_t, weight_t))
+    y = np.asarray(labels, dtype=np.int64)
+    N = Hs.shape[0]
+    rows = np.flatnonzero(y != ignore_index)
+    nv = int(rows.size)
+    tok = np.zeros(N)
+    lse_s = np.zeros(N)
+    lse_t = np.zeros(N)
+    if nv:
+        zs = Hs[rows] @ Ws.T
+        zt = Ht[rows] @ Wt.T
+        _, ls = _log_softmax_stats(zs)
+        _, lt = _log_softmax_stats(zt)
+        pt = np.exp(zt - lt[:, None])
+        tok[rows] = ls - (pt * zs).sum(axis=1)
+        lse_s[rows] = ls
+        lse_t[rows] = lt
+    total = float(tok.sum())
+    if reduction == "mean":
+        loss = total / nv if nv else 0.0
+    elif reduction in ("sum", "none"):
+        loss = total
+    else:
+        raise ValueError(reduction)
+    return {"loss": loss, "token_loss": tok, "lse_s": lse_s, "lse_t": lse_t, "n_valid": nv}
+
+
+def kd_backward(hidden_s, weight_s, hidden_t, weight_t, labels, ignore_index: int = IGNORE_INDEX,
+                reduction: str = "mean", grad_loss=1.0) -> dict:
+    """Student gradients of ``kd_forward``: dz_S = c (p_S - p_T); dH_S = dz_S W_S,
+    dW_S = dz_S^T H_S (the teacher gets none)."""
+    Hs, Ws, Ht, Wt = (_as_f64(a) for a in (hidden_s, weight_s, hidden_t, weight_t))
+    y = np.asarray(labels, dtype=np.int64)
+    rows = np.flatnonzero(y != ignore_index)
+    nv = int(rows.size)
+    c = _scale(reduction, nv, grad_loss, rows)
+    dH = np.zeros_like(Hs)
+    dW = np.zeros_like(Ws)
+    if nv:
+        zs = Hs[rows] @ Ws.T
+        zt = Ht[rows] @ Wt.T
+        _, ls = _log_softmax_stats(zs)
+        _, lt = _log_softmax_stats(zt)
+        G = np.exp(zs - ls[:, None]) - np.exp(zt - lt[:, None])
+        G *= c if np.ndim(c) == 0 else c[:, None]
+        dH[rows] = G @ Ws
+        dW = G.T @ Hs[rows]
+    return {"dH": dH, "dW": dW, "n_valid": nv}
 
 
 def adamw_step(theta, grad, exp_avg, exp_avg_sq, step: int, lr: float, beta1: float = 0.9,

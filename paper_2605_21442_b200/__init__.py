@@ -17,6 +17,7 @@ from .lce import (  # noqa: F401
     forward,
     forward_backward,
     fused_workspace_bytes,
+    kd_forward_backward,
     launch_count,
     linear_cross_entropy,
     make_problem,

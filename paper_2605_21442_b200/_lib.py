@@ -25,6 +25,7 @@ EXPORTS = [
     "lce_comm_get_unique_id", "lce_comm_init", "lce_comm_destroy", "lce_comm_size", "lce_comm_rank",
     "lce_status_string", "lce_abi_version", "lce_launch_count", "lce_profile_enable", "lce_profile_read",
     "lce_debug_gemm", "lce_fused_workspace_bytes", "lce_forward_backward", "lce_backward_adamw",
+    "lce_kd_workspace_bytes", "lce_kd_forward_backward",
 ]
 
 
@@ -74,6 +75,11 @@ def _load() -> ctypes.CDLL:
     lib.lce_backward_adamw.argtypes = [P(Problem), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, P(AdamW), vp,
                                        ctypes.c_size_t, vp]
     lib.lce_backward_adamw.restype = ctypes.c_int
+    lib.lce_kd_workspace_bytes.argtypes = [P(Problem), ctypes.c_int64]
+    lib.lce_kd_workspace_bytes.restype = ctypes.c_size_t
+    lib.lce_kd_forward_backward.argtypes = [P(Problem), ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                            ctypes.c_int, vp, ctypes.c_size_t, vp]
+    lib.lce_kd_forward_backward.restype = ctypes.c_int
     lib.lce_check_device_status.argtypes = [vp, vp]
     lib.lce_check_device_status.restype = ctypes.c_int
     lib.lce_comm_get_unique_id.argtypes = [ctypes.c_char_p]

@@ -49,6 +49,13 @@ struct GemmDims {
   // split-K: each output tile is computed as `ksplit` (<= 1: one) independent
   // k-ranges; the epilogue sees the split index and must reduce them itself
   int32_t ksplit;
+  // raster: output tiles are walked in groups of `group_m` M-blocks, N-blocks
+  // inner (0 = kGroupM); the concurrently resident tiles then share A and B
+  // tiles through L2
+  int32_t group_m;
+  // L2 eviction priority of the A / B operand loads (0 normal, 1 evict_first,
+  // 2 evict_last): operands reused by later tiles of the raster stay in L2
+  int32_t a_hint, b_hint;
 };
 
 // Geometry handed to the epilogue for one output tile.
@@ -71,21 +78,21 @@ __device__ __forceinline__ int extent(const int32_t* p, int32_t v, int32_t off, 
   return (cap > 0 && x > cap) ? cap : x;
 }
 
-__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
-  const int per_group = kGroupM * num_n;
+__device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int GM, int& m_blk, int& n_blk) {
+  const int per_group = GM * num_n;
   const int g = t / per_group;
-  const int first_m = g * kGroupM;
-  const int gsz = min(num_m - first_m, kGroupM);
+  const int first_m = g * GM;
+  const int gsz = min(num_m - first_m, GM);
   const int r = t - g * per_group;
   m_blk = first_m + r % gsz;
   n_blk = r / gsz;
 }
 
-__device__ __forceinline__ WorkItem work_of(int t, int num_m, int num_n, int S, int num_k) {
+__device__ __forceinline__ WorkItem work_of(int t, int num_m, int num_n, int S, int num_k, int GM) {
   WorkItem w;
   const int tile = t / S;
   w.s = t - tile * S;
-  tile_of(tile, num_m, num_n, w.mb, w.nb);
+  tile_of(tile, num_m, num_n, GM, w.mb, w.nb);
   w.kb0 = static_cast<int>(static_cast<long long>(num_k) * w.s / S);
   w.kb1 = static_cast<int>(static_cast<long long>(num_k) * (w.s + 1) / S);
   return w;
@@ -115,6 +122,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
+  const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
 
   if (warp == 0 && lane == 0) {
@@ -144,8 +152,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         const int m0 = w.mb * BM, n0 = w.nb * BN;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -154,16 +163,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* b = sB + stage * kBStageBytes;
           const int k0 = kb * BK;
           if (!A_MN) {
-            tma_load_2d(a, &tmA, &full[stage], k0, m0);
+            tma_load_2d_hint(a, &tmA, &full[stage], k0, m0, pa);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * BK * 128, &tmA, &full[stage], m0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d_hint(a + j * BK * 128, &tmA, &full[stage], m0 + 64 * j, k0, pa);
           }
           if (!B_MN) {
-            tma_load_2d(b, &tmB, &full[stage], k0, n0);
+            tma_load_2d_hint(b, &tmB, &full[stage], k0, n0, pb);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * BK * 128, &tmB, &full[stage], n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d_hint(b + j * BK * 128, &tmB, &full[stage], n0 + 64 * j, k0, pb);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -219,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+      const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
@@ -285,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_k = (K + BK - 1) / BK;
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
+  const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
 
   if (warp == 0 && lane == 0) {
@@ -314,8 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---------------------------------------------------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         const int ma = w.mb * kPairBM + 128 * rank;  // this CTA's A rows
         const int nbh = w.nb * BN + 128 * rank;      // this CTA's B rows (N half)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
@@ -325,16 +338,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* b = sB + stage * kHalf;
           const int k0 = kb * BK;
           if (!A_MN) {
-            tma_load_2d_pair(a, &tmA, &full[stage], k0, ma);
+            tma_load_2d_pair(a, &tmA, &full[stage], k0, ma, pa);
           } else {
-            tma_load_2d_pair(a, &tmA, &full[stage], ma, k0);
-            tma_load_2d_pair(a + BK * 128, &tmA, &full[stage], ma + 64, k0);
+            tma_load_2d_pair(a, &tmA, &full[stage], ma, k0, pa);
+            tma_load_2d_pair(a + BK * 128, &tmA, &full[stage], ma + 64, k0, pa);
           }
           if (!B_MN) {
-            tma_load_2d_pair(b, &tmB, &full[stage], k0, nbh);
+            tma_load_2d_pair(b, &tmB, &full[stage], k0, nbh, pb);
           } else {
-            tma_load_2d_pair(b, &tmB, &full[stage], nbh, k0);
-            tma_load_2d_pair(b + BK * 128, &tmB, &full[stage], nbh + 64, k0);
+            tma_load_2d_pair(b, &tmB, &full[stage], nbh, k0, pb);
+            tma_load_2d_pair(b + BK * 128, &tmB, &full[stage], nbh + 64, k0, pb);
           }
           if (++stage == kPairStages) {
             stage = 0;
@@ -352,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -391,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      const WorkItem w = work_of(t, num_m, num_n, S, num_k);
+      const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);

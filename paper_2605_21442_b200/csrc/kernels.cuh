@@ -264,7 +264,7 @@ struct EpiAdamW {
     int64_t ld;           // D
     const Header* hdr;    // c
     float lr, beta1, beta2, eps, decay;  // decay = 1 - lr * weight_decay
-    float step_size, inv_sqrt_bc2;       // lr / bc1, 1 / sqrt(bc2)
+    float step_size, sqrt_bc2;           // lr / bc1, sqrt(bc2)
   };
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
@@ -291,9 +291,9 @@ struct EpiAdamW {
         for (int e = 0; e < 4; ++e) {
           const float g = cs * x[4 * v + e];
           thv[e] = thv[e] * p.decay;
-          mv[e] = p.beta1 * mv[e] + (1.f - p.beta1) * g;
+          mv[e] = mv[e] + (1.f - p.beta1) * (g - mv[e]);  // torch: exp_avg.lerp_(grad, 1 - beta1)
           sv[e] = p.beta2 * sv[e] + (1.f - p.beta2) * g * g;
-          const float denom = __fsqrt_rn(sv[e]) * p.inv_sqrt_bc2 + p.eps;
+          const float denom = __fdiv_rn(__fsqrt_rn(sv[e]), p.sqrt_bc2) + p.eps;
           thv[e] = thv[e] - p.step_size * __fdiv_rn(mv[e], denom);
         }
         *reinterpret_cast<float4*>(p.theta + rowoff + col) = th;
@@ -588,10 +588,10 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
   const float lse = Mx + logf(S);
   const float l = lse - zt[r];
   const int i = idx[r];
-  lse_out[i] = lse;
+  if (lse_out) lse_out[i] = lse;
   if (tok_out) tok_out[i] = l;
   lse_c[r] = lse;
-  ltok[r] = l;
+  if (ltok) ltok[r] = l;
 }
 
 // S4 of the fused path without the recompute: the chunk's fp32 logits Z (kept
@@ -631,6 +631,68 @@ __global__ void __launch_bounds__(256) fixup_g_kernel(const float* __restrict__ 
       w[j / 2] = pack_bf16x2(g0, g1);
     }
     grow[v] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// NEXT-4 linear KD (forward KL, reading R23) for one row chunk, from the kept
+// fp32 student / teacher logits: G = s_i (p_S - p_T) in bf16 and
+// l_i = lse_S - sum_j p_T z_S (fixed-order block reduction).  One CTA per row.
+__global__ void __launch_bounds__(256) kd_fixup_kernel(const float* __restrict__ Zs, const float* __restrict__ Zt,
+                                                       int64_t ldz, int n_cols, int row_off, int cap,
+                                                       const float* __restrict__ lse_s, const float* __restrict__ lse_t,
+                                                       const float* __restrict__ row_scale, const Header* hdr,
+                                                       uint16_t* __restrict__ G, float* __restrict__ ltok,
+                                                       float* __restrict__ tok_out, const int32_t* __restrict__ idx) {
+  __shared__ float red[256];
+  const int m = blockIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= ((M + 63) & ~63)) return;
+  uint4* grow = reinterpret_cast<uint4*>(G + static_cast<int64_t>(m) * ldz);
+  const int nvec = static_cast<int>(ldz / 8);
+  if (m >= M) {
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) grow[v] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const int r = row_off + m;
+  const float lsl = lse_s[r] * kLog2e, ltl = lse_t[r] * kLog2e;
+  const float sc = hdr->c * (row_scale ? row_scale[r] : 1.f);
+  const float4* zs = reinterpret_cast<const float4*>(Zs + static_cast<int64_t>(m) * ldz);
+  const float4* zt = reinterpret_cast<const float4*>(Zt + static_cast<int64_t>(m) * ldz);
+  float acc = 0.f;
+  for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const float4 a0 = zs[2 * v], a1 = zs[2 * v + 1], b0 = zt[2 * v], b1 = zt[2 * v + 1];
+    const float xs[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float xt[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      float g[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int col = 8 * v + j + u;
+        if (col < n_cols) {
+          const float ps = ex2_approx(fmaf(xs[j + u], kLog2e, -lsl));
+          const float pt = ex2_approx(fmaf(xt[j + u], kLog2e, -ltl));
+          acc = fmaf(pt, xs[j + u], acc);
+          g[u] = sc * (ps - pt);
+        } else {
+          g[u] = 0.f;
+        }
+      }
+      w[j / 2] = pack_bf16x2(g[0], g[1]);
+    }
+    grow[v] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const float l = lse_s[r] - red[0];
+    ltok[r] = l;
+    if (tok_out) tok_out[idx[r]] = l;
   }
 }
 

@@ -140,6 +140,39 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
   return true;
 }
 
+// Linear KD (NEXT-4): the fused layout plus the teacher's rows, partials and
+// fp32 logit chunk; 10 bytes per chunk element (Z_S, Z_T fp32 + G bf16).
+struct KdPlan {
+  FusedPlan f;  // student (z = Z_S), G, partials, header/index sections
+  int64_t Dt;
+  size_t hct, pmt, pst, zt2, lset, total;
+};
+
+bool make_kd_plan(const lce_problem_t* p, int64_t teacher_dim, KdPlan* kp) {
+  if (teacher_dim <= 0 || teacher_dim % 8 != 0 || teacher_dim >= (1ll << 31)) return false;
+  lce_problem_t q = *p;
+  // the student plan sized for 10 bytes per element instead of 6
+  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
+  q.chunk_budget_bytes = budget * 6 / 10;
+  KdPlan k{};
+  if (!make_fused_plan(&q, &k.f)) return false;
+  k.Dt = teacher_dim;
+  size_t off = k.f.total;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = static_cast<size_t>(round_up(static_cast<int64_t>(off + bytes), 1024));
+    return o;
+  };
+  k.hct = take(static_cast<size_t>(k.f.n_chunks * k.f.Nc * teacher_dim * 2));
+  k.pmt = take(static_cast<size_t>(k.f.n_tiles * k.f.Nc * 4));
+  k.pst = take(static_cast<size_t>(k.f.n_tiles * k.f.Nc * 4));
+  k.zt2 = take(static_cast<size_t>(k.f.Nc * k.f.ldv * 4));
+  k.lset = take(static_cast<size_t>(k.f.cap * 4));
+  k.total = off;
+  *kp = k;
+  return true;
+}
+
 bool use_pair();
 
 // Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
@@ -318,9 +351,37 @@ bool use_pair() {
 // the 256-column tile.
 int b_box_rows() { return use_pair() ? BN / 2 : BN; }
 
+// Raster group (M-blocks per N sweep) of a GEMM class: the caller's choice,
+// overridable per class with LCE_GROUP_M_<class index> or globally with
+// LCE_GROUP_M (tuning experiments).
+int group_override(int cls, int dflt) {
+  char name[32];
+  snprintf(name, sizeof(name), "LCE_GROUP_M_%d", cls);
+  const char* e = getenv(name);
+  if (!e) e = getenv("LCE_GROUP_M");
+  return e ? atoi(e) : dflt;
+}
+
+int hint_override(int cls, char which, int dflt) {
+  char name[32];
+  snprintf(name, sizeof(name), "LCE_HINT_%c_%d", which, cls);
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 template <bool A_MN, bool B_MN, class Epi>
-lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d,
+lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d_in,
                          const typename Epi::Params& ep, int sms, cudaStream_t s) {
+  GemmDims d = d_in;
+  d.group_m = group_override(cls, d.group_m);
+  // L2 policy: in the forward / recompute GEMMs the A group (rows of H_c) is
+  // reused by every vocab tile of the sweep while each W tile is used once per
+  // group -> keep H_c, stream W.  Overridable: LCE_HINT_A_<cls> / LCE_HINT_B_<cls>.
+  // (Measured on B200: every combination within the +-2% run-to-run noise of
+  // these power-capped, MMA-bound kernels, evict_first on either operand
+  // 2-12% slower; default normal.)
+  d.a_hint = hint_override(cls, 'A', 0);
+  d.b_hint = hint_override(cls, 'B', 0);
   LaunchScope sc(cls, s);
   if (!use_pair()) {
     gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
@@ -578,7 +639,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
     GemmDims d{nullptr, static_cast<int32_t>(pl.Vl), nullptr, 0, static_cast<int32_t>(pl.D)};
     EpiAdamW::Params ep{adam->theta, adam->exp_avg, adam->exp_avg_sq, adam->w, pl.D, hdr, h.lr, h.beta1, h.beta2,
                         h.eps, 1.f - h.lr * h.weight_decay, static_cast<float>(h.lr / bc1),
-                        static_cast<float>(1.0 / sqrt(bc2))};
+                        static_cast<float>(sqrt(bc2))};
     return launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_any, t_any, d, ep, dev.sms, s);
   }
   const int N = static_cast<int>(pl.N);
@@ -654,7 +715,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
         const int64_t o = v0 * pl.D;
         EpiAdamW::Params ep{adam->theta + o, adam->exp_avg + o, adam->exp_avg_sq + o, adam->w + o, pl.D, hdr,
                             h.lr, h.beta1, h.beta2, h.eps, 1.f - h.lr * h.weight_decay,
-                            static_cast<float>(h.lr / bc1), static_cast<float>(1.0 / sqrt(bc2))};
+                            static_cast<float>(h.lr / bc1), static_cast<float>(sqrt(bc2))};
         LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
       }
     }
@@ -807,6 +868,140 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
       GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
       EpiDW::Params ep{dweight, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
       LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, dev.sms, s)));
+    }
+  }
+  {
+    LaunchScope sc(LCE_K_COMBINE, s);
+    loss_reduce_kernel<<<1, 1024, 0, s>>>(ltok, hdr, loss, n_valid, p->reduction);
+    LCE_TRY(last_error());
+  }
+  return LCE_OK;
+}
+
+size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim) {
+  KdPlan kp;
+  if (!p || !make_kd_plan(p, teacher_dim, &kp)) return 0;
+  return kp.total;
+}
+
+lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim, const uint16_t* hidden_s,
+                                     const uint16_t* weight_s, const uint16_t* hidden_t, const uint16_t* weight_t,
+                                     const int32_t* labels, const float* grad_loss, float* loss, float* token_loss,
+                                     int32_t* n_valid, uint16_t* dhidden_s, float* dweight_s, int accumulate_dweight,
+                                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (!p) return LCE_ERR_NULL;
+  if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
+  KdPlan kp;
+  if (!make_kd_plan(p, teacher_dim, &kp)) return LCE_ERR_SHAPE;
+  if (p->vocab_start != 0 || p->vocab_local != p->vocab_total) return LCE_ERR_COMM;
+  const FusedPlan& fp = kp.f;
+  if (!workspace || !weight_s || !weight_t || !loss || !dweight_s) return LCE_ERR_NULL;
+  if (fp.N > 0 && (!hidden_s || !hidden_t || !labels || !dhidden_s)) return LCE_ERR_NULL;
+  const void* ptrs[] = {hidden_s, weight_s, hidden_t, weight_t, labels, grad_loss, loss,
+                        token_loss, n_valid, dhidden_s, dweight_s, workspace};
+  for (const void* q : ptrs)
+    if (q && !aligned16(q)) return LCE_ERR_ALIGN;
+  if (workspace_bytes < kp.total) return LCE_ERR_WORKSPACE;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
+  if (fp.N == 0) {
+    LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
+    if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
+    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight_s, 0, fp.Vl * fp.D * sizeof(float), s));
+    return LCE_OK;
+  }
+  const int N = static_cast<int>(fp.N);
+  int32_t* idx = reinterpret_cast<int32_t*>(ws + fp.idx);
+  int32_t* yc = reinterpret_cast<int32_t*>(ws + fp.yc);
+  float* zt = reinterpret_cast<float*>(ws + fp.zt);
+  float* lse_s = reinterpret_cast<float*>(ws + fp.lsec);
+  float* lse_t = reinterpret_cast<float*>(ws + kp.lset);
+  float* gsc = reinterpret_cast<float*>(ws + fp.gsc);
+  float* ltok = reinterpret_cast<float*>(ws + fp.ltok);
+  uint16_t* hcs = reinterpret_cast<uint16_t*>(ws + fp.hc);
+  uint16_t* hct = reinterpret_cast<uint16_t*>(ws + kp.hct);
+  float* pms = reinterpret_cast<float*>(ws + fp.pm);
+  float* pss = reinterpret_cast<float*>(ws + fp.ps);
+  float* pmt = reinterpret_cast<float*>(ws + kp.pmt);
+  float* pst = reinterpret_cast<float*>(ws + kp.pst);
+  float* Zs = reinterpret_cast<float*>(ws + fp.z);
+  float* Zt = reinterpret_cast<float*>(ws + kp.zt2);
+  uint16_t* G = reinterpret_cast<uint16_t*>(ws + fp.g);
+  const float* row_grad = p->reduction == LCE_NONE ? grad_loss : nullptr;
+  // KD uses the labels only as the ignore mask (R23): no upper range check
+  const int64_t no_range = (1ll << 62);
+  {
+    LaunchScope sc(LCE_K_PREP, s);
+    prep_kernel<<<1, 1024, 0, s>>>(labels, N, p->ignore_index, no_range, idx, yc, zt, nullptr, token_loss, hdr,
+                                   grad_loss, p->reduction);
+    LCE_TRY(last_error());
+  }
+  {
+    LaunchScope sc(LCE_K_GATHER, s);
+    gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden_s, fp.D, N, idx, hdr, hcs, nullptr, nullptr,
+                                                               row_grad, gsc, labels, p->ignore_index, no_range,
+                                                               dhidden_s);
+    gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden_t, kp.Dt, N, idx, hdr, hct, nullptr, nullptr,
+                                                               nullptr, nullptr, labels, p->ignore_index, no_range,
+                                                               nullptr);
+    LCE_TRY(last_error());
+  }
+  const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
+  const int32_t Dt = static_cast<int32_t>(kp.Dt);
+  CUtensorMap t_ws_k, t_wt_k, t_ws_mn, t_g_k, t_g_mn;
+  LCE_TRY(map_kmajor(&t_ws_k, weight_s, fp.Vl, fp.D, fp.D, b_box_rows()));
+  LCE_TRY(map_kmajor(&t_wt_k, weight_t, fp.Vl, kp.Dt, kp.Dt, b_box_rows()));
+  LCE_TRY(map_mnmajor(&t_ws_mn, weight_s, fp.Vl, fp.D, fp.D));
+  LCE_TRY(map_kmajor(&t_g_k, G, fp.Nc, fp.ldv, fp.ldv, BM));
+  LCE_TRY(map_mnmajor(&t_g_mn, G, fp.Nc, fp.ldv, fp.ldv));
+  for (int64_t q = 0; q < fp.n_chunks; ++q) {
+    const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
+    const uint16_t* hsq = hcs + static_cast<int64_t>(r0) * fp.D;
+    const uint16_t* htq = hct + static_cast<int64_t>(r0) * kp.Dt;
+    CUtensorMap t_hs_k, t_hs_mn, t_ht_k;
+    LCE_TRY(map_kmajor(&t_hs_k, hsq, fp.Nc, fp.D, fp.D, BM));
+    LCE_TRY(map_mnmajor(&t_hs_mn, hsq, fp.Nc, fp.D, fp.D));
+    LCE_TRY(map_kmajor(&t_ht_k, htq, fp.Nc, kp.Dt, kp.Dt, BM));
+    {  // student and teacher logit chunks (kept in fp32) + their LSE partials
+      GemmDims ds{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
+      EpiLse::Params es{yc, 0, Vl, pms, pss, fp.Nc, zt, r0, Zs, fp.ldv};
+      LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_hs_k, t_ws_k, ds, es, dev.sms, s)));
+      GemmDims dt{&hdr->n_valid, 0, nullptr, Dt, Vl, r0, Nc, 0, 0};
+      EpiLse::Params et{yc, 0, Vl, pmt, pst, fp.Nc, zt, r0, Zt, fp.ldv};
+      LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_ht_k, t_wt_k, dt, et, dev.sms, s)));
+    }
+    {  // lse_S and lse_T of the chunk rows
+      LaunchScope sc(LCE_K_COMBINE, s);
+      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
+          pms, pss, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_s, nullptr);
+      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
+          pmt, pst, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_t, nullptr);
+      LCE_TRY(last_error());
+    }
+    {  // G = s_i (p_S - p_T), l_i = lse_S - E_{p_T}[z_S]
+      LaunchScope sc(LCE_K_BWD_G, s);
+      kd_fixup_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Zs, Zt, fp.ldv, Vl, r0, Nc, lse_s, lse_t,
+                                                                   row_grad ? gsc : nullptr, hdr, G, ltok,
+                                                                   token_loss, idx);
+      LCE_TRY(last_error());
+    }
+    {  // dH_S rows of the chunk (split-K into the dead Z_S), then dW_S
+      const int split = dh_split(fp, dev.sms);
+      GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
+      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden_s, idx, r0, 0, split > 1 ? Zs : nullptr, fp.Nc * fp.D};
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_ws_mn, d, ep, dev.sms, s)));
+      if (split > 1) {
+        LaunchScope sc(LCE_K_FINAL, s);
+        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Zs, split, fp.Nc * fp.D, fp.D, r0, Nc, idx,
+                                                                     hdr, dhidden_s);
+        LCE_TRY(last_error());
+      }
+      GemmDims dw{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
+      EpiDW::Params ew{dweight_s, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
+      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hs_mn, dw, ew, dev.sms, s)));
     }
   }
   {

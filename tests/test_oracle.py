@@ -430,3 +430,99 @@ def test_adamw_matches_torch_fp64_multi_step():
     np.testing.assert_allclose(th, p.detach().numpy(), rtol=1e-13, atol=1e-15)
     np.testing.assert_allclose(m, opt.state[p]["exp_avg"].numpy(), rtol=1e-13, atol=1e-16)
     np.testing.assert_allclose(v, opt.state[p]["exp_avg_sq"].numpy(), rtol=1e-13, atol=1e-18)
+
+
+# ---------------------------------------------------------------- KD loss (NEXT-4, R23)
+def _kd_problem(seed, N=40, Ds=6, Dt=9, V=23):
+    rng = np.random.default_rng(seed)
+    Hs, Ws = rng.standard_normal((N, Ds)), rng.standard_normal((V, Ds)) / math.sqrt(Ds)
+    Ht, Wt = rng.standard_normal((N, Dt)), rng.standard_normal((V, Dt)) / math.sqrt(Dt)
+    y = rng.integers(0, V, size=N)
+    y[rng.permutation(N)[:7]] = IGNORE_INDEX
+    return Hs, Ws, Ht, Wt, y
+
+
+def test_kd_teacher_equals_student():
+    """Same head for teacher and student: l_i = entropy of p_S and dz = p_S - p_T = 0."""
+    from oracle import kd_backward, kd_forward
+
+    Hs, Ws, _, _, y = _kd_problem(20)
+    f = kd_forward(Hs, Ws, Hs, Ws, y)
+    z = Hs @ Ws.T
+    p = np.exp(z - z.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    ent = -(p * np.log(p)).sum(1)
+    valid = y != IGNORE_INDEX
+    np.testing.assert_allclose(f["token_loss"][valid], ent[valid], rtol=1e-12)
+    b = kd_backward(Hs, Ws, Hs, Ws, y)
+    assert np.abs(b["dH"]).max() < 1e-15 and np.abs(b["dW"]).max() < 1e-15
+
+
+def test_kd_uniform_teacher_closed_form():
+    """W_T = 0: p_T uniform, l_i = lse_S(i) - mean_j z_S(i, j)."""
+    from oracle import kd_forward
+
+    Hs, Ws, Ht, Wt, y = _kd_problem(21)
+    f = kd_forward(Hs, Ws, Ht, np.zeros_like(Wt), y, reduction="sum")
+    z = Hs @ Ws.T
+    lse = np.log(np.exp(z).sum(1))
+    valid = y != IGNORE_INDEX
+    assert f["loss"] == pytest.approx((lse - z.mean(1))[valid].sum(), rel=1e-13)
+
+
+def test_kd_one_hot_teacher_is_cross_entropy():
+    """A teacher sharply peaked on y_i (spike Delta = 60) reduces KD to the CE
+    of the student (up to e^-60)."""
+    from oracle import kd_forward
+
+    Hs, Ws, _, _, y = _kd_problem(22)
+    N, V = len(y), Ws.shape[0]
+    Ht = np.eye(N)                       # one teacher feature per token
+    Wt = np.zeros((V, N))
+    for i, lab in enumerate(y):
+        if lab != IGNORE_INDEX:
+            Wt[lab, i] = 60.0
+    f = kd_forward(Hs, Ws, Ht, Wt, y)
+    ce = lce_forward(Hs, Ws, y)
+    assert f["loss"] == pytest.approx(ce["loss"], rel=1e-12)
+
+
+@pytest.mark.parametrize("reduction", ["mean", "sum"])
+def test_kd_matches_torch_fp64(reduction):
+    """P10-style: -(softmax(z_T) * log_softmax(z_S)).sum(-1) over non-ignored
+    rows with torch autograd (CPU fp64) for the student gradients."""
+    from oracle import kd_backward, kd_forward
+
+    Hs, Ws, Ht, Wt, y = _kd_problem(23)
+    hs = torch.tensor(Hs, requires_grad=True)
+    ws = torch.tensor(Ws, requires_grad=True)
+    zt = torch.tensor(Ht) @ torch.tensor(Wt).T
+    per = -(torch.softmax(zt, -1) * torch.log_softmax(hs @ ws.T, -1)).sum(-1)
+    mask = torch.tensor(y != IGNORE_INDEX)
+    L = per[mask].sum() / (mask.sum() if reduction == "mean" else 1)
+    L.backward()
+    f = kd_forward(Hs, Ws, Ht, Wt, y, reduction=reduction)
+    b = kd_backward(Hs, Ws, Ht, Wt, y, reduction=reduction)
+    assert f["loss"] == pytest.approx(L.item(), rel=1e-12)
+    np.testing.assert_allclose(b["dH"], hs.grad.numpy(), rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(b["dW"], ws.grad.numpy(), rtol=1e-10, atol=1e-15)
+
+
+def test_kd_finite_differences():
+    """P4 for KD: every student gradient entry at a tiny shape."""
+    from oracle import kd_backward, kd_forward
+
+    Hs, Ws, Ht, Wt, y = _kd_problem(24, N=6, Ds=3, Dt=4, V=5)
+    b = kd_backward(Hs, Ws, Ht, Wt, y)
+    for arr, grad, name in ((Hs, b["dH"], "H"), (Ws, b["dW"], "W")):
+        for idx in np.ndindex(arr.shape):
+            eps = 1e-6 * max(1.0, abs(arr[idx]))
+            ap, am = arr.copy(), arr.copy()
+            ap[idx] += eps
+            am[idx] -= eps
+            if name == "H":
+                fp, fm = kd_forward(ap, Ws, Ht, Wt, y)["loss"], kd_forward(am, Ws, Ht, Wt, y)["loss"]
+            else:
+                fp, fm = kd_forward(Hs, ap, Ht, Wt, y)["loss"], kd_forward(Hs, am, Ht, Wt, y)["loss"]
+            fd = (fp - fm) / (2 * eps)
+            assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (name, idx)
