@@ -88,10 +88,13 @@ __device__ __forceinline__ void tile_of(int t, int num_m, int num_n, int GM, int
   n_blk = r / gsz;
 }
 
+// Split index outermost: concurrently resident work items share one k-range,
+// so (with an N-fastest raster) each A k-slab is read once for all N tiles.
 __device__ __forceinline__ WorkItem work_of(int t, int num_m, int num_n, int S, int num_k, int GM) {
   WorkItem w;
-  const int tile = t / S;
-  w.s = t - tile * S;
+  const int tiles = num_m * num_n;
+  w.s = t / tiles;
+  const int tile = t - w.s * tiles;
   tile_of(tile, num_m, num_n, GM, w.mb, w.nb);
   w.kb0 = static_cast<int>(static_cast<long long>(num_k) * w.s / S);
   w.kb1 = static_cast<int>(static_cast<long long>(num_k) * (w.s + 1) / S);

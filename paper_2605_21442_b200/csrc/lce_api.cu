@@ -373,6 +373,11 @@ template <bool A_MN, bool B_MN, class Epi>
 lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d_in,
                          const typename Epi::Params& ep, int sms, cudaStream_t s) {
   GemmDims d = d_in;
+  // dH / dW have few N tiles (N = D) and long K: an N-fastest raster
+  // (group_m = 1) lets the concurrently resident tiles of one A row block
+  // read each A k-slab once; the forward / recompute GEMMs (N = V) keep
+  // 16-row-block groups so the H_c group stays in L2 while W streams.
+  if (d.group_m == 0) d.group_m = (cls == LCE_K_BWD_DH || cls == LCE_K_BWD_DW) ? 1 : kGroupM;
   d.group_m = group_override(cls, d.group_m);
   // L2 policy: in the forward / recompute GEMMs the A group (rows of H_c) is
   // reused by every vocab tile of the sweep while each W tile is used once per

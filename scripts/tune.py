@@ -66,7 +66,7 @@ def main():
                 configs.append({f"LCE_HINT_A_{K[c]}": str(ha), f"LCE_HINT_B_{K[c]}": str(hb)})
     if a.sweep in ("group", "both"):
         for c in classes:
-            for g in (2, 4, 8, 32, 64):
+            for g in (1, 2, 4, 8, 16, 32):
                 configs.append({f"LCE_GROUP_M_{K[c]}": str(g)})
     base = None
     for cfg in configs:
