@@ -21,7 +21,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -185,8 +184,8 @@ def main():
     ap.add_argument("--chunk-budget", type=int, default=0,
                     help="chunk_budget_bytes (fused: logit+G chunk bytes, default 4 GiB; split: G chunk, 512 MiB)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "split"],
-                    help="fused = lce_forward_backward (no recompute, 1 GPU); split = lce_forward + lce_backward "
-                         "(recompute; vocab-parallel); auto = fused on 1 GPU, split otherwise")
+                    help="fused = lce_forward_backward (no logit recompute, 6 N_v V D flops); split = "
+                         "lce_forward + lce_backward (recompute from lse, 8 N_v V D flops); auto = fused")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -224,12 +223,12 @@ def main():
     dH = torch.empty_like(H)
     dW = torch.empty(vl, D, dtype=torch.float32, device=dev)
 
-    fused = args.path == "fused" or (args.path == "auto" and world == 1)
+    fused = args.path in ("fused", "auto")
 
     def run_path(Hx, Wx, yx):
         if fused:  # lce_forward_backward: logits kept per row chunk, 6 N_v V D flops
             F.forward_backward(Hx, Wx, yx, dhidden=dH, dweight=dW, workspace=ws, out=out,
-                               chunk_budget_bytes=args.chunk_budget)
+                               chunk_budget_bytes=args.chunk_budget, comm=comm, vocab_start=vstart, vocab_total=V)
         else:      # lce_forward + lce_backward: recompute from lse, 8 N_v V D flops
             F.forward(Hx, Wx, yx, comm=comm, vocab_start=vstart, vocab_total=V, workspace=ws, out=out,
                       chunk_budget_bytes=args.chunk_budget)

@@ -165,8 +165,10 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
  * dW GEMMs: 6 N_v V D flops instead of 8.  The upstream gradient must be
  * known up front (grad_loss as in lce_backward; NULL = 1).  dW is accumulated
  * across row chunks in fp32.  Nc is set by chunk_budget_bytes (bytes of the
- * fp32 + bf16 chunk buffers; 0 = 4 GiB).  comm must be NULL
- * (LCE_ERR_COMM otherwise): vocab-parallel runs use lce_forward/lce_backward. */
+ * fp32 + bf16 chunk buffers; 0 = 4 GiB).  With comm != NULL (vocab-parallel,
+ * P:180) each row chunk's (max, sum-exp, target logit) are combined with the
+ * same MAX / SUM all-reduces as lce_forward, and the chunk's fp32 dH partial is
+ * all-reduced on the communicator's side stream while the dW GEMM runs. */
 size_t lce_fused_workspace_bytes(const lce_problem_t* p);
 lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
                                   const uint16_t* hidden, const uint16_t* weight,

@@ -594,6 +594,46 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
   if (ltok) ltok[r] = l;
 }
 
+// Vocab-parallel S3 of one row chunk (fused path):
+//   mode 1: local partials -> m_loc, m_glob (= m_loc, MAX-reduced next), s, z_t copy
+//   mode 2: after MAX all-reduce: s *= exp(m_loc - M)   (SUM-reduced next, with z_t)
+//   mode 3: after SUM all-reduce: lse = M + ln s, l = lse - z_t -> outputs, lse_c, ltok
+// Chunk buffers are indexed by chunk row m; [s | z_t] are adjacent (one all-reduce).
+__global__ void __launch_bounds__(256) combine_chunk_vp_kernel(int mode, const float* __restrict__ pm,
+                                                               const float* __restrict__ ps, int n_tiles, int64_t ld,
+                                                               int row_off, int cap, const float* __restrict__ zt,
+                                                               float* __restrict__ m_loc, float* __restrict__ m_glob,
+                                                               float* __restrict__ sz, const int32_t* __restrict__ idx,
+                                                               const Header* hdr, float* __restrict__ lse_out,
+                                                               float* __restrict__ tok_out, float* __restrict__ lse_c,
+                                                               float* __restrict__ ltok) {
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= M) return;
+  const int r = row_off + m;
+  if (mode == 1) {
+    float Mx = -INFINITY, S = 0.f;
+    for (int t = 0; t < n_tiles; ++t) Mx = fmaxf(Mx, pm[t * ld + m]);
+    for (int t = 0; t < n_tiles; ++t) S += ps[t * ld + m] * expf(pm[t * ld + m] - Mx);
+    m_loc[m] = Mx;
+    m_glob[m] = Mx;
+    sz[m] = S;
+    sz[cap + m] = zt[r];
+    return;
+  }
+  if (mode == 2) {
+    sz[m] *= expf(m_loc[m] - m_glob[m]);
+    return;
+  }
+  const float lse = m_glob[m] + logf(sz[m]);
+  const float l = lse - sz[cap + m];
+  const int i = idx[r];
+  if (lse_out) lse_out[i] = lse;
+  if (tok_out) tok_out[i] = l;
+  lse_c[r] = lse;
+  ltok[r] = l;
+}
+
 // S4 of the fused path without the recompute: the chunk's fp32 logits Z (kept
 // from the forward GEMM) -> G = s_i (exp(z - lse_i) - [j == y_i]) in bf16,
 // s_i = c (MEAN / SUM) or g_i (NONE); rows in [M, ceil64(M)) and columns
@@ -698,13 +738,31 @@ __global__ void __launch_bounds__(256) kd_fixup_kernel(const float* __restrict__
 
 // Split-K dH of a row chunk: dhidden[idx[row_off + m]] = bf16(sum_s part[s][m])
 // (c already folded into G), fixed split order.  One CTA per row.
+// With out_f32 != null (vocab-parallel) the fp32 sum goes to out_f32[m] instead
+// (all-reduced across ranks, then cast/scattered by a second ksplit = 1 call).
 __global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict__ part, int ksplit,
                                                         int64_t part_stride, int64_t D, int row_off, int cap,
                                                         const int32_t* __restrict__ idx, const Header* hdr,
-                                                        uint16_t* __restrict__ dhidden) {
+                                                        uint16_t* __restrict__ dhidden,
+                                                        float* __restrict__ out_f32 = nullptr) {
   const int m = blockIdx.x;
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= M) return;
+  if (out_f32) {
+    float4* o = reinterpret_cast<float4*>(out_f32 + static_cast<int64_t>(m) * D);
+    for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
+      float4 a = reinterpret_cast<const float4*>(part + static_cast<int64_t>(m) * D)[v];
+      for (int s = 1; s < ksplit; ++s) {
+        const float4 b = reinterpret_cast<const float4*>(part + s * part_stride + static_cast<int64_t>(m) * D)[v];
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      o[v] = a;
+    }
+    return;
+  }
   uint2* dst = reinterpret_cast<uint2*>(dhidden + static_cast<int64_t>(idx[row_off + m]) * D);
   for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
     float4 a = reinterpret_cast<const float4*>(part + static_cast<int64_t>(m) * D)[v];

@@ -98,7 +98,9 @@ constexpr int64_t kDefaultFusedBudget = 4ll << 30;
 
 struct FusedPlan {
   int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
-  size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, total;
+  size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g;
+  size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
+  size_t total;
 };
 
 bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
@@ -135,6 +137,10 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
   q.ps = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
   q.z = take(static_cast<size_t>(q.Nc * q.ldv * 4));
   q.g = take(static_cast<size_t>(q.Nc * q.ldv * 2));
+  q.vmloc = take(static_cast<size_t>(q.Nc * 4));
+  q.vmglob = take(static_cast<size_t>(q.Nc * 4));
+  q.vsz = take(static_cast<size_t>(q.Nc * 8));
+  q.vdh = take(static_cast<size_t>(q.Nc * q.D * 4));  // fp32 dH chunk (vocab-parallel only)
   q.total = off;
   *fp = q;
   return true;
@@ -776,8 +782,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   FusedPlan fp;
   if (!make_fused_plan(p, &fp)) return LCE_ERR_SHAPE;
-  if (comm) return LCE_ERR_COMM;  // vocab-parallel runs through lce_forward + lce_backward
-  if (p->vocab_start != 0 || p->vocab_local != p->vocab_total) return LCE_ERR_COMM;
+  if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
   if (!workspace || !weight || !loss || !dweight) return LCE_ERR_NULL;
   if (fp.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
   const void* ptrs[] = {hidden, weight, labels, grad_loss, loss, lse, token_loss, n_valid, dhidden, dweight, workspace};
@@ -807,6 +812,10 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
   float* ps = reinterpret_cast<float*>(ws + fp.ps);
   float* Z = reinterpret_cast<float*>(ws + fp.z);
   uint16_t* G = reinterpret_cast<uint16_t*>(ws + fp.g);
+  float* vmloc = reinterpret_cast<float*>(ws + fp.vmloc);
+  float* vmglob = reinterpret_cast<float*>(ws + fp.vmglob);
+  float* vsz = reinterpret_cast<float*>(ws + fp.vsz);
+  float* vdh = reinterpret_cast<float*>(ws + fp.vdh);
   const float* row_grad = p->reduction == LCE_NONE ? grad_loss : nullptr;
 
   {
@@ -840,11 +849,34 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
       EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, Z, fp.ldv};
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
-    {  // S3 for the chunk rows
+    const unsigned cb = static_cast<unsigned>(fp.Nc / 256);
+    if (!comm) {  // S3 for the chunk rows
       LaunchScope sc(LCE_K_COMBINE, s);
-      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
-          pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse, token_loss, lsec, ltok);
+      combine_rows_kernel<<<cb, 256, 0, s>>>(pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse,
+                                            token_loss, lsec, ltok);
       LCE_TRY(last_error());
+    } else {  // vocab-parallel S3: MAX of m, rescale, SUM of (s, z_t) over the chunk rows
+      const int nt = static_cast<int>(fp.n_tiles);
+      {
+        LaunchScope sc(LCE_K_COMBINE, s);
+        combine_chunk_vp_kernel<<<cb, 256, 0, s>>>(1, pm, ps, nt, fp.Nc, r0, Nc, zt, vmloc, vmglob, vsz, idx, hdr,
+                                                   lse, token_loss, lsec, ltok);
+        LCE_TRY(last_error());
+      }
+      LCE_TRY(allreduce(comm, vmglob, static_cast<size_t>(fp.Nc), ncclMax, s));
+      {
+        LaunchScope sc(LCE_K_COMBINE, s);
+        combine_chunk_vp_kernel<<<cb, 256, 0, s>>>(2, pm, ps, nt, fp.Nc, r0, Nc, zt, vmloc, vmglob, vsz, idx, hdr,
+                                                   lse, token_loss, lsec, ltok);
+        LCE_TRY(last_error());
+      }
+      LCE_TRY(allreduce(comm, vsz, static_cast<size_t>(2 * fp.Nc), ncclSum, s));
+      {
+        LaunchScope sc(LCE_K_COMBINE, s);
+        combine_chunk_vp_kernel<<<cb, 256, 0, s>>>(3, pm, ps, nt, fp.Nc, r0, Nc, zt, vmloc, vmglob, vsz, idx, hdr,
+                                                   lse, token_loss, lsec, ltok);
+        LCE_TRY(last_error());
+      }
     }
     {  // S4 without recompute: G = s_i (softmax - onehot) from the kept logits
       LaunchScope sc(LCE_K_BWD_G, s);
@@ -859,13 +891,22 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
     {
       const int split = dh_split(fp, dev.sms);
       GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
-      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, split > 1 ? Z : nullptr, fp.Nc * fp.D};
+      // vocab-parallel: the partial dH always goes through fp32 (slabs in Z, or
+      // straight into the chunk accumulator) so it can be all-reduced
+      float* part = split > 1 ? Z : (comm ? vdh : nullptr);
+      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
       LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
       if (split > 1) {
         LaunchScope sc(LCE_K_FINAL, s);
         reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                     dhidden);
+                                                                     dhidden, comm ? vdh : nullptr);
         LCE_TRY(last_error());
+      }
+      if (comm) {  // S7: sum the chunk's dH over ranks on the side stream, overlapping the dW GEMM
+        LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
+        LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
+        LCE_TRY(allreduce(comm, vdh, static_cast<size_t>(fp.Nc * fp.D), ncclSum, comm->side));
+        LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
       }
     }
     // S5: dW (+)= G_q^T H_q (K = chunk rows)
@@ -873,6 +914,13 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
       GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
       EpiDW::Params ep{dweight, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
       LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, dev.sms, s)));
+    }
+    if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
+      LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
+      LaunchScope sc(LCE_K_FINAL, s);
+      reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(vdh, 1, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+                                                                   dhidden);
+      LCE_TRY(last_error());
     }
   }
   {

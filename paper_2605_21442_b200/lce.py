@@ -213,14 +213,15 @@ def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.T
                      with_token_loss: bool = False, dhidden: Optional[torch.Tensor] = None,
                      dweight: Optional[torch.Tensor] = None, accumulate_dweight: bool = False,
                      workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0, stream=None,
-                     out: Optional[dict] = None) -> dict:
+                     out: Optional[dict] = None, comm: Optional[Comm] = None, vocab_start: int = 0,
+                     vocab_total: Optional[int] = None) -> dict:
     """Fused forward + backward without logit recompute (lce_forward_backward).
 
     Returns {loss, lse, n_valid, token_loss, dhidden, dweight}."""
     _check_inputs(hidden, weight, labels)
     N, D = hidden.shape
-    prob = make_problem(N, D, weight.shape[0], ignore_index=ignore_index, reduction=reduction,
-                        chunk_budget_bytes=chunk_budget_bytes)
+    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
     need = fused_workspace_bytes(prob)
     if need == 0:
@@ -244,7 +245,8 @@ def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.T
         grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
         if grad_loss.numel() != (N if reduction == "none" else 1):
             raise ValueError("grad_loss must have N elements for 'none' and 1 otherwise")
-    check(lib.lce_forward_backward(ctypes.byref(prob), None, _ptr(hidden), _ptr(weight), _ptr(labels),
+    check(lib.lce_forward_backward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
+                                   _ptr(labels),
                                    _ptr(grad_loss), _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["token_loss"]),
                                    _ptr(out["n_valid"]), _ptr(dhidden), _ptr(dweight),
                                    1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)),

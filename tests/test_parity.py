@@ -388,6 +388,26 @@ def test_fused_none_accumulate_and_empty(cuda_lib):
     assert allign["loss"] == 0 and not allign["dH"].any() and not allign["dW"].any()
 
 
+def test_fused_single_rank_communicator_path(cuda_lib):
+    """Vocab-parallel fused path (per-chunk MAX/SUM all-reduces, fp32 dH chunk
+    all-reduced on the side stream) on a one-rank NCCL communicator."""
+    import paper_2605_21442_b200 as F
+
+    comm = F.Comm.single()
+    try:
+        lab = packed_labels(2048, 3000, seed=2)[:900]
+        inp = small(900, 128, 3000, labels=lab)
+        out = F.forward_backward(inp.hidden, inp.weight, inp.labels, with_token_loss=True, comm=comm,
+                                 chunk_budget_bytes=256 * 6 * 3072)
+        torch.cuda.synchronize()
+        g = {"loss": out["loss"].item(), "n_valid": int(out["n_valid"].item()),
+             "lse": out["lse"].cpu().double().numpy(), "tok": out["token_loss"].cpu().double().numpy(),
+             "dH": out["dhidden"].float().cpu().double().numpy(), "dW": out["dweight"].cpu().double().numpy()}
+        assert_parity(g, oracle_run(inp), lab)
+    finally:
+        comm.close()
+
+
 def test_fused_matches_recompute_path(cuda_lib):
     """Same inputs through lce_forward + lce_backward and lce_forward_backward:
     identical lse/loss (same forward GEMM), gradients within bf16 rounding."""
