@@ -61,7 +61,7 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   if (vc > round_up(Vl, BN)) vc = round_up(Vl, BN);
   q.Vc = vc;
   q.n_chunks = ceil_div(Vl, vc);
-  q.nblocks = ceil_div(q.cap, 256);
+  q.nblocks = ceil_div(q.cap, kRowsPerCta);  // combine: one warp per row
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -849,7 +849,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
       EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, Z, fp.ldv};
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
-    const unsigned cb = static_cast<unsigned>(fp.Nc / 256);
+    const unsigned cb = static_cast<unsigned>(fp.Nc / kRowsPerCta);
     if (!comm) {  // S3 for the chunk rows
       LaunchScope sc(LCE_K_COMBINE, s);
       combine_rows_kernel<<<cb, 256, 0, s>>>(pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse,
@@ -1028,9 +1028,9 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim
     }
     {  // lse_S and lse_T of the chunk rows
       LaunchScope sc(LCE_K_COMBINE, s);
-      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
+      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / kRowsPerCta), 256, 0, s>>>(
           pms, pss, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_s, nullptr);
-      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / 256), 256, 0, s>>>(
+      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / kRowsPerCta), 256, 0, s>>>(
           pmt, pst, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_t, nullptr);
       LCE_TRY(last_error());
     }

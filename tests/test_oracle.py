@@ -90,6 +90,13 @@ def test_softmax_minus_onehot_rows_sum_to_zero():
     assert np.abs(col).max() < 1e-14 * max(1.0, np.abs(b["dW"]).max() * 50)
 
 
+def test_bilinear_identity_between_dH_and_dW():
+    """P11: z = H W^T is bilinear, so <H, dH> = sum_ij G_ij z_ij = <W, dW>."""
+    H, W, y = rand_problem(70, 9, 40, 25)
+    b = lce_backward(H, W, y, reduction="sum")
+    assert (H * b["dH"]).sum() == pytest.approx((W * b["dW"]).sum(), rel=1e-12)
+
+
 # ---------------------------------------------------------------- P3 ignore rows
 def test_ignored_rows_never_touch_the_projection():
     """P3 / P:166 mask-first: NaN/Inf garbage in ignored rows of H changes

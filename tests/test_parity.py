@@ -408,6 +408,44 @@ def test_fused_single_rank_communicator_path(cuda_lib):
         comm.close()
 
 
+@pytest.mark.parametrize("path", ["split", "fused"])
+def test_vocab_shard_offsets_single_rank(cuda_lib, path):
+    """A one-rank communicator over a vocab SHARD (vocab_start > 0, labels
+    global, some outside the shard): the GPU computes exactly the shard
+    statistics of P:180's loss parallel -- oracle shard_stats / shard_backward
+    (lse of the shard, target logit only from the owning shard, G without the
+    onehot for foreign labels)."""
+    import paper_2605_21442_b200 as F
+    from oracle import shard_backward, shard_stats
+
+    V, D, v0, vl = 1000, 128, 384, 500
+    inp = small(300, D, V, seed=17)
+    Wsh = inp.weight[v0:v0 + vl].contiguous()
+    comm = F.Comm.single()
+    try:
+        if path == "split":
+            out = F.forward(inp.hidden, Wsh, inp.labels, comm=comm, vocab_start=v0, vocab_total=V,
+                            with_token_loss=True)
+            dh, dw = F.backward(inp.hidden, Wsh, inp.labels, out["lse"], comm=comm, vocab_start=v0, vocab_total=V)
+        else:
+            out = F.forward_backward(inp.hidden, Wsh, inp.labels, comm=comm, vocab_start=v0, vocab_total=V,
+                                     with_token_loss=True, chunk_budget_bytes=256 * 6 * 512)
+            dh, dw = out["dhidden"], out["dweight"]
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    H, W, y = np_inputs(inp)
+    st = shard_stats(H, W[v0:v0 + vl], y, v0, V)
+    valid = st["valid"]
+    lse_sh = np.where(valid, st["m"] + np.log(np.where(valid, st["s"], 1.0)), 0.0)
+    tok_sh = np.where(valid, lse_sh - st["z_target"], 0.0)
+    assert np.abs(out["lse"].cpu().double().numpy() - lse_sh).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
+    assert np.abs(out["token_loss"].cpu().double().numpy() - tok_sh).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
+    sb = shard_backward(H, W[v0:v0 + vl], y, v0, lse_sh, 1.0 / int(valid.sum()))
+    assert fro_rel(dh.float().cpu().double().numpy(), sb["dH_partial"]) <= GRAD_TOL
+    assert fro_rel(dw.cpu().double().numpy(), sb["dW_shard"]) <= GRAD_TOL
+
+
 def test_fused_matches_recompute_path(cuda_lib):
     """Same inputs through lce_forward + lce_backward and lce_forward_backward:
     identical lse/loss (same forward GEMM), gradients within bf16 rounding."""
@@ -537,13 +575,19 @@ def test_kd_many_chunks_none_and_self_distillation(cuda_lib):
 
 
 # ------------------------------------------------------------ full size, bench launch configuration
-@pytest.mark.parametrize("name", ["llama8b", "qwen7b"])
-def test_full_size_sampled_rows_and_invariants(cuda_lib, name):
-    """At the bench's full size: sampled rows (lse, token loss, dH) vs the
-    oracle row by row; loss == mean of token losses; sum_j dW_j ~ 0 (P2)."""
+@pytest.mark.parametrize("name,path", [("llama8b", "fused"), ("llama8b", "split"), ("qwen7b", "fused"),
+                                       ("qwen7b", "split"), ("llama1b", "fused"), ("llama70b", "fused")])
+def test_full_size_sampled_rows_and_invariants(cuda_lib, name, path):
+    """At full size in the bench's launch configuration (fused = bench default):
+    sampled rows (lse, token loss, dH) vs the oracle row by row; loss == mean
+    of token losses; sum_j dW_j ~ 0 (P2); <H, dH> == <W, dW> (P11)."""
     inp = make_config(name, device="cuda")
-    g = gpu_run(inp)
+    g = fused_run(inp) if path == "fused" else gpu_run(inp)
     H, W, y = np_inputs(inp)
+    # P11: z is bilinear in (H, W), so sum_i h_i.dH_i = sum_ij G_ij z_ij = sum_j w_j.dW_j
+    hdh = float((inp.hidden.double() * torch.from_numpy(g["dH"]).to("cuda")).sum())
+    wdw = float((inp.weight.double() * torch.from_numpy(g["dW"]).to("cuda")).sum())
+    assert abs(hdh - wdw) <= 2e-2 * max(abs(hdh), abs(wdw)), (hdh, wdw)
     rng = np.random.default_rng(0)
     rows = np.sort(rng.choice(len(y), size=48, replace=False))
     rows = np.concatenate([rows, [0, len(y) - 1]])
