@@ -196,6 +196,7 @@ def main():
         return reference_arm(args, rank)
 
     import paper_2605_21442_b200 as F
+    from paper_2605_21442_b200.dist import max_over_ranks
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -260,12 +261,9 @@ def main():
     F.profile_enable(False)
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-        if dist:
-            dist.barrier()
+    if dist:  # the job's step time is the slowest rank's (device time, max over ranks)
+        ms = max_over_ranks(ms, device=dev)
+        dist.barrier()
     peak_hbm = torch.cuda.max_memory_allocated(dev)
     ms_step = ms / args.steps
     value = nv * args.steps / (ms / 1e3)
@@ -322,9 +320,7 @@ def main():
         torch.cuda.synchronize()
         ems = a.elapsed_time(b)
         if dist:
-            t = torch.tensor([ems], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = t.item()
+            ems = max_over_ranks(ems, device=dev)
         e2e = {"value": nv * args.steps / (ems / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": H.numel() * 2 + W.numel() * 2 + y.numel() * 4, "d2h_bytes_per_step": 4,
                "ms_per_step": ems / args.steps}

@@ -446,6 +446,46 @@ def test_vocab_shard_offsets_single_rank(cuda_lib, path):
     assert fro_rel(dw.cpu().double().numpy(), sb["dW_shard"]) <= GRAD_TOL
 
 
+@pytest.mark.parametrize("path", ["split", "fused"])
+def test_cuda_graph_capture_replays_bitwise(cuda_lib, path):
+    """Every launch is stream-ordered with no host sync or allocation, so a
+    whole fwd+bwd step can be captured in a CUDA graph and replayed."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(700, 256, 5000, seed=18)
+    h, w, y = inp.hidden, inp.weight, inp.labels
+    ws = F.Workspace()
+    out = {"loss": torch.empty(1, device="cuda"), "lse": torch.empty(700, device="cuda"),
+           "n_valid": torch.empty(1, dtype=torch.int32, device="cuda"), "token_loss": None}
+    dH = torch.empty_like(h)
+    dW = torch.empty(w.shape, dtype=torch.float32, device="cuda")
+
+    def step():
+        if path == "fused":
+            F.forward_backward(h, w, y, dhidden=dH, dweight=dW, workspace=ws, out=out,
+                               chunk_budget_bytes=256 * 6 * 5120)
+        else:
+            F.forward(h, w, y, workspace=ws, out=out)
+            F.backward(h, w, y, out["lse"], dhidden=dH, dweight=dW, workspace=ws, chunk_budget_bytes=700 * 2 * 1024)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    ref = [out["loss"].clone(), out["lse"].clone(), dH.clone(), dW.clone()]
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    for t in (out["loss"], out["lse"], dH, dW):
+        t.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, [out["loss"], out["lse"], dH, dW]):
+        assert torch.equal(a, b)
+
+
 def test_fused_matches_recompute_path(cuda_lib):
     """Same inputs through lce_forward + lce_backward and lce_forward_backward:
     identical lse/loss (same forward GEMM), gradients within bf16 rounding."""
@@ -576,7 +616,8 @@ def test_kd_many_chunks_none_and_self_distillation(cuda_lib):
 
 # ------------------------------------------------------------ full size, bench launch configuration
 @pytest.mark.parametrize("name,path", [("llama8b", "fused"), ("llama8b", "split"), ("qwen7b", "fused"),
-                                       ("qwen7b", "split"), ("llama1b", "fused"), ("llama70b", "fused")])
+                                       ("qwen7b", "split"), ("llama1b", "fused"), ("llama70b", "fused"),
+                                       ("llama70b", "split")])
 def test_full_size_sampled_rows_and_invariants(cuda_lib, name, path):
     """At full size in the bench's launch configuration (fused = bench default):
     sampled rows (lse, token loss, dH) vs the oracle row by row; loss == mean
