@@ -9,6 +9,7 @@ The oracle always consumes the exact bf16 values the GPU consumed.
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -494,6 +495,30 @@ def test_fused_matches_recompute_path(cuda_lib):
     np.testing.assert_array_equal(a["lse"], b["lse"])
     assert abs(a["loss"] - b["loss"]) <= 1e-6 * abs(a["loss"])
     assert fro_rel(b["dH"], a["dH"]) <= 5e-3 and fro_rel(b["dW"], a["dW"]) <= 5e-3
+
+
+# ------------------------------------------------------------ randomized shapes (property test)
+def test_random_shapes_all_paths(cuda_lib):
+    """40 seeded random problems (N in [1, 700], D in 8..264 step 8, V in [1, 3000],
+    random ignore fraction, both reductions, both GEMM variants, random chunk
+    budgets) through the split and fused paths, each against the oracle."""
+    rng = np.random.default_rng(2024)
+    for case in range(40):
+        N = int(rng.integers(1, 700))
+        D = int(8 * rng.integers(1, 34))
+        V = int(rng.integers(1, 3000))
+        frac = float(rng.choice([0.0, 0.1, 0.5, 0.95]))
+        red = str(rng.choice(["mean", "sum"]))
+        os.environ["LCE_GEMM"] = str(rng.choice(["pair", "single"]))
+        try:
+            inp = small(N, D, V, seed=100 + case, ignore_frac=frac)
+            o = oracle_run(inp, red)
+            lab = inp.labels.cpu().numpy()
+            budget = int(rng.choice([0, 256 * 2 * 512, 256 * 6 * 1024]))
+            assert_parity(gpu_run(inp, red, budget=budget), o, lab)
+            assert_parity(fused_run(inp, red, budget=budget), o, lab)
+        finally:
+            del os.environ["LCE_GEMM"]
 
 
 # ------------------------------------------------------------ NEXT-2: AdamW in the dW epilogue
