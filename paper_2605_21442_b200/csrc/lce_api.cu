@@ -55,7 +55,12 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.Vl = Vl;
   q.cap = round_up(N > 0 ? N : 1, kPairBM);  // whole 256-row pair tiles (G rows are written per tile)
   q.n_tiles = ceil_div(Vl, BN);
-  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultChunkBudget;
+  // Default G chunk: 512 MiB, but never fewer than 4096 vocab columns: every
+  // chunk re-reads and re-writes the fp32 dH accumulator (8 N D bytes), so for
+  // long contexts (App. A, ~1M tokens) the chunk grows with N instead.
+  const int64_t budget = p->chunk_budget_bytes > 0
+                             ? p->chunk_budget_bytes
+                             : (kDefaultChunkBudget > q.cap * 2 * 4096 ? kDefaultChunkBudget : q.cap * 2 * 4096);
   int64_t vc = (budget / (q.cap * 2)) / BN * BN;
   if (vc < BN) vc = BN;
   if (vc > round_up(Vl, BN)) vc = round_up(Vl, BN);

@@ -33,6 +33,9 @@ CONFIGS = {
     "llama8b": dict(N=16384, D=4096, V=128256, labels="uniform", ignore_frac=0.0, k=2),
     "qwen7b": dict(N=16384, D=3584, V=152064, labels="packed", ignore_frac=None, k=3),
     "llama70b": dict(N=65536, D=8192, V=128256, labels="uniform", ignore_frac=0.0, k=4),
+    # App. A: ~1M-token context-parallel samples on a Llama 3.2 model,
+    # where the loss phase was the peak-memory phase; 1B head shape, packed SFT labels
+    "llama1b_1m": dict(N=1048576, D=2048, V=128256, labels="packed", ignore_frac=None, k=5),
 }
 
 
