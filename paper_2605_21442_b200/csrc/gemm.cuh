@@ -67,6 +67,18 @@ struct TileInfo {
   int split;      // split-K index of this work item
 };
 
+// Epilogue policies derive from EpiBase; `prefetch` runs before the epilogue
+// waits for the tile's accumulator (i.e. while the MMA is still computing it),
+// so read-modify-write epilogues can pull their old output rows into L2 early.
+struct EpiBase {
+  template <class P>
+  static __device__ __forceinline__ void prefetch(const P&, const TileInfo&) {}
+};
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<uint64_t>(p)));
+}
+
 // One work item of the persistent schedule: output tile (mb, nb) and its k-block range.
 struct WorkItem {
   int mb, nb, s, kb0, kb1;
@@ -234,10 +246,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
+      TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s};
+      Epi::prefetch(ep, ti);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s};
       Epi::apply(ep, taddr, ti);
       tc_fence_before();
       __syncwarp();
@@ -408,11 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
+      TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
+                  w.kb1 == w.kb0, w.s};
+      Epi::prefetch(ep, ti);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
-      TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
-                  w.kb1 == w.kb0, w.s};
       Epi::apply(ep, taddr, ti);
       tc_fence_before();
       __syncwarp();

@@ -30,7 +30,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // -inf), and the target logit if the row's label falls in this tile.
 // Writes the partials (m, s) of tile column n_blk; the logits never leave
 // the SM.  (the dense [B,S,V] tensor is never materialised.)
-struct EpiLse {
+struct EpiLse : EpiBase {
   struct Params {
     const int32_t* yc;    // [N_v] compacted labels (global vocab ids)
     int32_t label_off;    // global vocab id of GEMM column 0
@@ -100,7 +100,7 @@ struct EpiLse {
 // RNE, into the vocab chunk buffer G_c[row, col].  Rows >= N_v and columns
 // >= n_cols are written as exact zeros so the next two GEMMs can run over
 // whole k-blocks.
-struct EpiG {
+struct EpiG : EpiBase {
   struct Params {
     const int32_t* yc;
     const float* lse_c;   // [N_v] lse of compacted rows
@@ -141,7 +141,7 @@ struct EpiG {
 // acc = (G_c W_c)[row, cols] for vocab chunk k.  Chunks are summed unscaled
 // in fp32 (acc_buf); on the last chunk (single GPU) the sum is scaled by c,
 // rounded to bf16 and scattered to dhidden[idx[row]] directly.
-struct EpiDH {
+struct EpiDH : EpiBase {
   struct Params {
     float* acc_buf;        // [rows_cap][ld] fp32 running sum over chunks
     int64_t ld;            // D
@@ -155,6 +155,13 @@ struct EpiDH {
     float* part;           // split-K: fp32 partial slabs [ksplit][rows][ld] (reduced by reduce_dh_kernel)
     int64_t part_stride;   // elements per slab
   };
+  // pull the running fp32 sum of this tile's row into L2 while the MMA runs
+  static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    if (p.part || p.first || r >= t.M) return;
+    const float* row = p.acc_buf + static_cast<int64_t>(p.row_off + r) * p.ld;
+    for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
+  }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
@@ -210,7 +217,7 @@ struct EpiDH {
 
 // ============================================================ S5 dW epilogue
 // acc = (G_c^T H)[vocab row, cols]; dW rows of the chunk = c * acc (or +=).
-struct EpiDW {
+struct EpiDW : EpiBase {
   struct Params {
     float* dW;            // chunk row 0 of dweight
     int64_t ld;           // D
@@ -218,6 +225,13 @@ struct EpiDW {
     const Header* hdr;
     int32_t use_c;        // 1: scale by c; 0: c already folded into G
   };
+  // accumulate mode reads the old dW tile row: pull it into L2 while the MMA runs
+  static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    if (!p.accumulate || t.zero_acc || r >= t.M) return;
+    const float* row = p.dW + static_cast<int64_t>(r) * p.ld;
+    for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
+  }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     if (t.zero_acc && p.accumulate) return;  // K == 0 adds nothing (uniform across the CTA)
     const int r = t.m0 + t.row;
@@ -255,7 +269,7 @@ struct EpiDW {
 // exists.  torch.optim.AdamW order: theta *= 1 - lr wd;
 // m = b1 m + (1 - b1) g; v = b2 v + (1 - b2) g^2;
 // theta -= (lr / bc1) m / (sqrt(v) / sqrt(bc2) + eps); W = bf16(theta).
-struct EpiAdamW {
+struct EpiAdamW : EpiBase {
   struct Params {
     float* theta;         // fp32 master weights, chunk row 0
     float* exp_avg;
@@ -266,6 +280,17 @@ struct EpiAdamW {
     float lr, beta1, beta2, eps, decay;  // decay = 1 - lr * weight_decay
     float step_size, sqrt_bc2;           // lr / bc1, sqrt(bc2)
   };
+  // theta, m, v rows of the tile are read-modify-written: pull them into L2 early
+  static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
+    const int r = t.m0 + t.row;
+    if (r >= t.M) return;
+    const int64_t o = static_cast<int64_t>(r) * p.ld;
+    for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) {
+      prefetch_l2(p.theta + o + t.n0 + 32 * c);
+      prefetch_l2(p.exp_avg + o + t.n0 + 32 * c);
+      prefetch_l2(p.exp_avg_sq + o + t.n0 + 32 * c);
+    }
+  }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
@@ -307,7 +332,7 @@ struct EpiAdamW {
 };
 
 // ============================================================ diagnostics epilogue
-struct EpiStore {
+struct EpiStore : EpiBase {
   struct Params {
     float* C;
     int64_t ldc;
