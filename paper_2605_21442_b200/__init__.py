@@ -9,6 +9,7 @@ from ._lib import LIB_PATH, LceError, lib  # noqa: F401  (raises ImportError if 
 from .lce import (  # noqa: F401
     Comm,
     LinearCrossEntropyFunction,
+    LinearCrossEntropyFusedFunction,
     Workspace,
     backward,
     backward_adamw,

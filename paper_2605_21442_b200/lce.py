@@ -324,7 +324,35 @@ class LinearCrossEntropyFunction(torch.autograd.Function):
         return dh, dw.to(weight.dtype), None, None, None
 
 
-def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduction: str = "mean"):
+class LinearCrossEntropyFusedFunction(torch.autograd.Function):
+    """autograd wrapper over lce_forward_backward: the gradients for an upstream
+    gradient of 1 are produced together with the loss (no logit recompute) and
+    scaled by the actual upstream scalar in backward (MEAN / SUM are linear in it)."""
+
+    @staticmethod
+    def forward(ctx, hidden, weight, labels, ignore_index, reduction):
+        out = forward_backward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)
+        ctx.save_for_backward(out["dhidden"], out["dweight"])
+        ctx.wdtype = weight.dtype
+        return out["loss"].reshape(())
+
+    @staticmethod
+    def backward(ctx, g):
+        dh, dw = ctx.saved_tensors
+        if not torch.equal(g, torch.ones_like(g)):  # the common loss.backward() case needs no rescale
+            dh = (dh.float() * g).to(dh.dtype)
+            dw = dw * g
+        return dh, dw.to(ctx.wdtype), None, None, None
+
+
+def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduction: str = "mean",
+                         fused: bool = False):
+    """loss = CE(hidden @ weight^T, labels) (P:166 LCE).  fused=True computes the
+    gradients in the forward call without the logit recompute (MEAN / SUM only)."""
+    if fused:
+        if reduction == "none":
+            raise ValueError("fused autograd needs a scalar loss (reduction 'mean' or 'sum')")
+        return LinearCrossEntropyFusedFunction.apply(hidden, weight, labels, ignore_index, reduction)
     return LinearCrossEntropyFunction.apply(hidden, weight, labels, ignore_index, reduction)
 
 

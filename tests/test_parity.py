@@ -87,6 +87,26 @@ def assert_parity(g, o, labels, ignore=IGNORE):
     assert np.all(g["dH"][ign] == 0)
 
 
+# ------------------------------------------------------------ the C ABI from plain C
+def test_plain_c_client(cuda_lib, tmp_path):
+    """tests/c_abi_check.c drives liblce.so through include/lce.h only (cudaMalloc
+    buffers, no Python / torch) on the closed-form W = 0 case (P1)."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2605_21442_b200")
+    exe = str(tmp_path / "c_abi_check")
+    cuda = "/usr/local/cuda"
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"), "-I", f"{cuda}/include",
+                    os.path.join(root, "tests", "c_abi_check.c"), "-o", exe, "-L", pkg, "-llce",
+                    f"-Wl,-rpath,{pkg}", "-L", f"{cuda}/lib64", "-lcudart", f"-Wl,-rpath,{cuda}/lib64", "-lm"],
+                   check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 2
+
+
 # ------------------------------------------------------------ mainloop descriptors
 @pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (296, 520, 200), (64, 40, 16), (136, 264, 72)])
@@ -299,6 +319,25 @@ def test_none_reduction_per_token_logprobs(cuda_lib, variant, N, D, V):
     assert fro_rel(dh.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
     assert fro_rel(dw.cpu().double().numpy(), b["dW"]) <= GRAD_TOL
     assert np.all(dh.float().cpu().numpy()[y == IGNORE] == 0)
+
+
+@pytest.mark.parametrize("scale", [1.0, -0.5])
+def test_autograd_fused(cuda_lib, scale):
+    """fused=True: gradients produced in the forward call, scaled by the
+    upstream scalar in backward."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(300, 64, 1000, seed=19)
+    h = inp.hidden.clone().requires_grad_(True)
+    w = inp.weight.clone().requires_grad_(True)
+    loss = F.linear_cross_entropy(h, w, inp.labels, fused=True)
+    (loss * scale).backward()
+    H, W, y = np_inputs(inp)
+    o = lce_forward(H, W, y)
+    b = lce_backward(H, W, y, grad_loss=scale)
+    assert abs(loss.item() - o["loss"]) <= LOSS_TOL * abs(o["loss"])
+    assert fro_rel(h.grad.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
+    assert fro_rel(w.grad.float().cpu().double().numpy(), b["dW"]) <= 2e-2
 
 
 def test_autograd_none_reduction(cuda_lib):
