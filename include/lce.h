@@ -189,9 +189,12 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
  *   p->hidden_dim = D_S, teacher_dim = D_T (% 8 == 0); hidden_s [N, D_S],
  *   weight_s [V, D_S], hidden_t [N, D_T], weight_t [V, D_T] (bf16);
  *   grad_loss / loss / token_loss / n_valid as lce_forward_backward.
- * One GPU only (vocab_local == vocab_total). */
+ * With comm != NULL both heads are vocab-sharded alike (weight_s / weight_t
+ * hold rows [vocab_start, vocab_start + V_l)): lse_S and lse_T are combined
+ * with MAX / SUM all-reduces, sum_j p_T z_S with a SUM all-reduce, and the
+ * chunk's dH_S partial is all-reduced as in lce_forward_backward. */
 size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim);
-lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim,
+lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, int64_t teacher_dim,
                                      const uint16_t* hidden_s, const uint16_t* weight_s,
                                      const uint16_t* hidden_t, const uint16_t* weight_t,
                                      const int32_t* labels, const float* grad_loss,

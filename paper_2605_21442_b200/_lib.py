@@ -77,8 +77,8 @@ def _load() -> ctypes.CDLL:
     lib.lce_backward_adamw.restype = ctypes.c_int
     lib.lce_kd_workspace_bytes.argtypes = [P(Problem), ctypes.c_int64]
     lib.lce_kd_workspace_bytes.restype = ctypes.c_size_t
-    lib.lce_kd_forward_backward.argtypes = [P(Problem), ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                                            ctypes.c_int, vp, ctypes.c_size_t, vp]
+    lib.lce_kd_forward_backward.argtypes = [P(Problem), vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                            vp, ctypes.c_int, vp, ctypes.c_size_t, vp]
     lib.lce_kd_forward_backward.restype = ctypes.c_int
     lib.lce_check_device_status.argtypes = [vp, vp]
     lib.lce_check_device_status.restype = ctypes.c_int

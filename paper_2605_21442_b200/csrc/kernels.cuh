@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(256) combine_chunk_vp_kernel(int mode, const f
   if (lse_out) lse_out[i] = lse;
   if (tok_out) tok_out[i] = l;
   lse_c[r] = lse;
-  ltok[r] = l;
+  if (ltok) ltok[r] = l;
 }
 
 // S4 of the fused path without the recompute: the chunk's fp32 logits Z (kept
@@ -730,7 +730,10 @@ __global__ void __launch_bounds__(256) kd_fixup_kernel(const float* __restrict__
                                                        const float* __restrict__ lse_s, const float* __restrict__ lse_t,
                                                        const float* __restrict__ row_scale, const Header* hdr,
                                                        uint16_t* __restrict__ G, float* __restrict__ ltok,
-                                                       float* __restrict__ tok_out, const int32_t* __restrict__ idx) {
+                                                       float* __restrict__ tok_out, const int32_t* __restrict__ idx,
+                                                       float* __restrict__ partial = nullptr) {
+  // partial != null (vocab-parallel): write this shard's sum_j p_T z_S to
+  // partial[m] instead of the loss (summed over ranks, then kd_loss_rows_kernel)
   __shared__ float red[256];
   const int m = blockIdx.x;
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
@@ -778,10 +781,29 @@ __global__ void __launch_bounds__(256) kd_fixup_kernel(const float* __restrict__
     __syncthreads();
   }
   if (threadIdx.x == 0) {
+    if (partial) {
+      partial[m] = red[0];
+      return;
+    }
     const float l = lse_s[r] - red[0];
     ltok[r] = l;
     if (tok_out) tok_out[idx[r]] = l;
   }
+}
+
+// Vocab-parallel KD loss of the chunk rows: l_i = lse_S - (all-reduced) E_{p_T}[z_S].
+__global__ void __launch_bounds__(256) kd_loss_rows_kernel(const float* __restrict__ e_sum,
+                                                           const float* __restrict__ lse_s, int row_off, int cap,
+                                                           const Header* hdr, float* __restrict__ ltok,
+                                                           float* __restrict__ tok_out,
+                                                           const int32_t* __restrict__ idx) {
+  const int m = blockIdx.x * 256 + threadIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  if (m >= M) return;
+  const int r = row_off + m;
+  const float l = lse_s[r] - e_sum[m];
+  ltok[r] = l;
+  if (tok_out) tok_out[idx[r]] = l;
 }
 
 // Split-K dH of a row chunk: dhidden[idx[row_off + m]] = bf16(sum_s part[s][m])

@@ -942,16 +942,17 @@ size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim) {
   return kp.total;
 }
 
-lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim, const uint16_t* hidden_s,
-                                     const uint16_t* weight_s, const uint16_t* hidden_t, const uint16_t* weight_t,
-                                     const int32_t* labels, const float* grad_loss, float* loss, float* token_loss,
-                                     int32_t* n_valid, uint16_t* dhidden_s, float* dweight_s, int accumulate_dweight,
-                                     void* workspace, size_t workspace_bytes, void* stream) {
+lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, int64_t teacher_dim,
+                                     const uint16_t* hidden_s, const uint16_t* weight_s, const uint16_t* hidden_t,
+                                     const uint16_t* weight_t, const int32_t* labels, const float* grad_loss,
+                                     float* loss, float* token_loss, int32_t* n_valid, uint16_t* dhidden_s,
+                                     float* dweight_s, int accumulate_dweight, void* workspace,
+                                     size_t workspace_bytes, void* stream) {
   if (!p) return LCE_ERR_NULL;
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   KdPlan kp;
   if (!make_kd_plan(p, teacher_dim, &kp)) return LCE_ERR_SHAPE;
-  if (p->vocab_start != 0 || p->vocab_local != p->vocab_total) return LCE_ERR_COMM;
+  if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
   const FusedPlan& fp = kp.f;
   if (!workspace || !weight_s || !weight_t || !loss || !dweight_s) return LCE_ERR_NULL;
   if (fp.N > 0 && (!hidden_s || !hidden_t || !labels || !dhidden_s)) return LCE_ERR_NULL;
@@ -977,6 +978,10 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim
   float* zt = reinterpret_cast<float*>(ws + fp.zt);
   float* lse_s = reinterpret_cast<float*>(ws + fp.lsec);
   float* lse_t = reinterpret_cast<float*>(ws + kp.lset);
+  float* vmloc = reinterpret_cast<float*>(ws + fp.vmloc);
+  float* vmglob = reinterpret_cast<float*>(ws + fp.vmglob);
+  float* vsz = reinterpret_cast<float*>(ws + fp.vsz);
+  float* vdh = reinterpret_cast<float*>(ws + fp.vdh);
   float* gsc = reinterpret_cast<float*>(ws + fp.gsc);
   float* ltok = reinterpret_cast<float*>(ws + fp.ltok);
   uint16_t* hcs = reinterpret_cast<uint16_t*>(ws + fp.hc);
@@ -1025,41 +1030,81 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, int64_t teacher_dim
     LCE_TRY(map_kmajor(&t_ht_k, htq, fp.Nc, kp.Dt, kp.Dt, BM));
     {  // student and teacher logit chunks (kept in fp32) + their LSE partials
       GemmDims ds{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
-      EpiLse::Params es{yc, 0, Vl, pms, pss, fp.Nc, zt, r0, Zs, fp.ldv};
+      const int32_t voff = static_cast<int32_t>(p->vocab_start);
+      EpiLse::Params es{yc, voff, Vl, pms, pss, fp.Nc, zt, r0, Zs, fp.ldv};
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_hs_k, t_ws_k, ds, es, dev.sms, s)));
       GemmDims dt{&hdr->n_valid, 0, nullptr, Dt, Vl, r0, Nc, 0, 0};
-      EpiLse::Params et{yc, 0, Vl, pmt, pst, fp.Nc, zt, r0, Zt, fp.ldv};
+      EpiLse::Params et{yc, voff, Vl, pmt, pst, fp.Nc, zt, r0, Zt, fp.ldv};
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_ht_k, t_wt_k, dt, et, dev.sms, s)));
     }
-    {  // lse_S and lse_T of the chunk rows
+    const unsigned cb = static_cast<unsigned>(fp.Nc / kRowsPerCta);
+    const int nt = static_cast<int>(fp.n_tiles);
+    if (!comm) {  // lse_S and lse_T of the chunk rows
       LaunchScope sc(LCE_K_COMBINE, s);
-      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / kRowsPerCta), 256, 0, s>>>(
-          pms, pss, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_s, nullptr);
-      combine_rows_kernel<<<static_cast<unsigned>(fp.Nc / kRowsPerCta), 256, 0, s>>>(
-          pmt, pst, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_t, nullptr);
+      combine_rows_kernel<<<cb, 256, 0, s>>>(pms, pss, nt, fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_s,
+                                            nullptr);
+      combine_rows_kernel<<<cb, 256, 0, s>>>(pmt, pst, nt, fp.Nc, r0, Nc, zt, idx, hdr, nullptr, nullptr, lse_t,
+                                            nullptr);
       LCE_TRY(last_error());
+    } else {  // vocab-parallel: global lse_S, then lse_T (MAX / rescale / SUM each)
+      const float* pmx[2] = {pms, pmt};
+      const float* psx[2] = {pss, pst};
+      float* lsex[2] = {lse_s, lse_t};
+      for (int h = 0; h < 2; ++h) {
+        for (int mode = 1; mode <= 3; ++mode) {
+          {
+            LaunchScope sc(LCE_K_COMBINE, s);
+            combine_chunk_vp_kernel<<<cb, 256, 0, s>>>(mode, pmx[h], psx[h], nt, fp.Nc, r0, Nc, zt, vmloc, vmglob,
+                                                       vsz, idx, hdr, nullptr, nullptr, lsex[h], nullptr);
+            LCE_TRY(last_error());
+          }
+          if (mode == 1) LCE_TRY(allreduce(comm, vmglob, static_cast<size_t>(fp.Nc), ncclMax, s));
+          if (mode == 2) LCE_TRY(allreduce(comm, vsz, static_cast<size_t>(2 * fp.Nc), ncclSum, s));
+        }
+      }
     }
-    {  // G = s_i (p_S - p_T), l_i = lse_S - E_{p_T}[z_S]
+    {  // G = s_i (p_S - p_T), l_i = lse_S - E_{p_T}[z_S] (vocab-parallel: E summed over ranks first)
       LaunchScope sc(LCE_K_BWD_G, s);
       kd_fixup_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Zs, Zt, fp.ldv, Vl, r0, Nc, lse_s, lse_t,
                                                                    row_grad ? gsc : nullptr, hdr, G, ltok,
-                                                                   token_loss, idx);
+                                                                   token_loss, idx, comm ? vsz : nullptr);
       LCE_TRY(last_error());
     }
-    {  // dH_S rows of the chunk (split-K into the dead Z_S), then dW_S
+    if (comm) {
+      LCE_TRY(allreduce(comm, vsz, static_cast<size_t>(fp.Nc), ncclSum, s));
+      LaunchScope sc(LCE_K_COMBINE, s);
+      kd_loss_rows_kernel<<<static_cast<unsigned>(ceil_div(fp.Nc, 256)), 256, 0, s>>>(vsz, lse_s, r0, Nc, hdr, ltok,
+                                                                                     token_loss, idx);
+      LCE_TRY(last_error());
+    }
+    {  // dH_S rows of the chunk (split-K into the dead Z_S; vocab-parallel: fp32 + all-reduce), then dW_S
       const int split = dh_split(fp, dev.sms);
       GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
-      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden_s, idx, r0, 0, split > 1 ? Zs : nullptr, fp.Nc * fp.D};
+      float* part = split > 1 ? Zs : (comm ? vdh : nullptr);
+      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden_s, idx, r0, 0, part, fp.Nc * fp.D};
       LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_ws_mn, d, ep, dev.sms, s)));
       if (split > 1) {
         LaunchScope sc(LCE_K_FINAL, s);
         reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Zs, split, fp.Nc * fp.D, fp.D, r0, Nc, idx,
-                                                                     hdr, dhidden_s);
+                                                                     hdr, dhidden_s, comm ? vdh : nullptr);
         LCE_TRY(last_error());
+      }
+      if (comm) {
+        LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
+        LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
+        LCE_TRY(allreduce(comm, vdh, static_cast<size_t>(fp.Nc * fp.D), ncclSum, comm->side));
+        LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
       }
       GemmDims dw{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
       EpiDW::Params ew{dweight_s, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
       LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hs_mn, dw, ew, dev.sms, s)));
+      if (comm) {
+        LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
+        LaunchScope sc(LCE_K_FINAL, s);
+        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(vdh, 1, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+                                                                     dhidden_s);
+        LCE_TRY(last_error());
+      }
     }
   }
   {

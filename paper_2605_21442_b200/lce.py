@@ -259,7 +259,9 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
                         weight_t: torch.Tensor, labels: torch.Tensor, *, grad_loss: Optional[torch.Tensor] = None,
                         ignore_index: int = -100, reduction: str = "mean", dhidden: Optional[torch.Tensor] = None,
                         dweight: Optional[torch.Tensor] = None, accumulate_dweight: bool = False,
-                        workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0, stream=None) -> dict:
+                        workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0, stream=None,
+                        comm: Optional[Comm] = None, vocab_start: int = 0,
+                        vocab_total: Optional[int] = None) -> dict:
     """Linear KD loss (forward KL, teacher -> student) and student gradients
     (lce_kd_forward_backward).  Returns {loss, token_loss, n_valid, dhidden, dweight}."""
     _check_inputs(hidden_s, weight_s, labels)
@@ -268,8 +270,8 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
     Dt = hidden_t.shape[1]
     if hidden_t.shape[0] != N or weight_t.shape[0] != weight_s.shape[0]:
         raise ValueError("teacher / student shapes disagree")
-    prob = make_problem(N, D, weight_s.shape[0], ignore_index=ignore_index, reduction=reduction,
-                        chunk_budget_bytes=chunk_budget_bytes)
+    prob = make_problem(N, D, weight_s.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden_s.device
     need = int(lib.lce_kd_workspace_bytes(ctypes.byref(prob), Dt))
     if need == 0:
@@ -286,7 +288,8 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
         dweight = torch.empty(weight_s.shape, dtype=torch.float32, device=dev)
     if grad_loss is not None:
         grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
-    check(lib.lce_kd_forward_backward(ctypes.byref(prob), Dt, _ptr(hidden_s), _ptr(weight_s), _ptr(hidden_t),
+    check(lib.lce_kd_forward_backward(ctypes.byref(prob), comm.handle if comm else None, Dt, _ptr(hidden_s),
+                                      _ptr(weight_s), _ptr(hidden_t),
                                       _ptr(weight_t), _ptr(labels), _ptr(grad_loss), _ptr(out["loss"]),
                                       _ptr(out["token_loss"]), _ptr(out["n_valid"]), _ptr(dhidden), _ptr(dweight),
                                       1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)),

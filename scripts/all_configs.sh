@@ -1,5 +1,5 @@
 # One bench line per BASELINE config and path (1 GPU): the table in BASELINE.md section 5.
-for cfg in llama1b llama8b qwen7b llama70b; do
+for cfg in llama1b llama8b qwen7b llama70b llama1b_1m; do
   for path in fused split; do
     echo "== $cfg $path"
     timeout 600 python bench.py --config $cfg --path $path --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "

@@ -678,6 +678,35 @@ def test_kd_many_chunks_none_and_self_distillation(cuda_lib):
     assert out["dhidden"].abs().max().item() == 0 and out["dweight"].abs().max().item() == 0
 
 
+def test_kd_vocab_shard_single_rank(cuda_lib):
+    """KD under a one-rank communicator over a vocab shard: the softmaxes run
+    over the shard's vocabulary only, so the result is kd_forward/kd_backward
+    of the shard's heads (exercises the MAX/SUM exchanges and the fp32 dH
+    all-reduce path)."""
+    import paper_2605_21442_b200 as F
+    from oracle import kd_backward, kd_forward
+
+    V, v0, vl = 3000, 1000, 1500
+    s, t = _kd_inputs(500, 128, 64, V, seed=20)
+    Ws = s.weight[v0:v0 + vl].contiguous()
+    Wt = t.weight[v0:v0 + vl].contiguous()
+    comm = F.Comm.single()
+    try:
+        out = F.kd_forward_backward(s.hidden, Ws, t.hidden, Wt, s.labels, comm=comm, vocab_start=v0, vocab_total=V,
+                                    chunk_budget_bytes=256 * 10 * 1536)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    Hs, _, y = np_inputs(s)
+    Ht = t.hidden.float().cpu().numpy()
+    Wsn, Wtn = Ws.float().cpu().numpy(), Wt.float().cpu().numpy()
+    f = kd_forward(Hs, Wsn, Ht, Wtn, y)
+    b = kd_backward(Hs, Wsn, Ht, Wtn, y)
+    assert abs(out["loss"].item() - f["loss"]) <= LOSS_TOL * abs(f["loss"])
+    assert fro_rel(out["dhidden"].float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
+    assert fro_rel(out["dweight"].cpu().double().numpy(), b["dW"]) <= GRAD_TOL
+
+
 # ------------------------------------------------------------ full size, bench launch configuration
 @pytest.mark.parametrize("name,path", [("llama8b", "fused"), ("llama8b", "split"), ("qwen7b", "fused"),
                                        ("qwen7b", "split"), ("llama1b", "fused"), ("llama70b", "fused"),
