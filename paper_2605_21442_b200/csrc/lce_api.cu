@@ -55,12 +55,17 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.Vl = Vl;
   q.cap = round_up(N > 0 ? N : 1, kPairBM);  // whole 256-row pair tiles (G rows are written per tile)
   q.n_tiles = ceil_div(Vl, BN);
-  // Default G chunk: 512 MiB, but never fewer than 4096 vocab columns: every
-  // chunk re-reads and re-writes the fp32 dH accumulator (8 N D bytes), so for
-  // long contexts (App. A, ~1M tokens) the chunk grows with N instead.
-  const int64_t budget = p->chunk_budget_bytes > 0
-                             ? p->chunk_budget_bytes
-                             : (kDefaultChunkBudget > q.cap * 2 * 4096 ? kDefaultChunkBudget : q.cap * 2 * 4096);
+  // Default G chunk: 16384 vocab columns, as bytes clamped to [512 MiB, 4 GiB],
+  // and never fewer than 4096 columns.  Every chunk re-reads and re-writes
+  // the fp32 dH accumulator (8 N D bytes) against 6 N V_c D flops of GEMMs, so
+  // wide chunks keep that traffic small; for ~1M-token contexts (App. A) the
+  // 4 GiB cap and the 4096-column floor bound the chunk instead.
+  int64_t budget = p->chunk_budget_bytes;
+  if (budget <= 0) {
+    budget = q.cap * 2 * 16384;
+    budget = budget < kDefaultChunkBudget ? kDefaultChunkBudget : (budget > (4ll << 30) ? (4ll << 30) : budget);
+    if (budget < q.cap * 2 * 4096) budget = q.cap * 2 * 4096;
+  }
   int64_t vc = (budget / (q.cap * 2)) / BN * BN;
   if (vc < BN) vc = BN;
   if (vc > round_up(Vl, BN)) vc = round_up(Vl, BN);
