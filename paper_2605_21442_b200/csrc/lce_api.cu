@@ -751,6 +751,51 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
   return LCE_OK;
 }
 
+// S6 + S5 (+ S7 under vocab parallel) of one row chunk of the fused paths (CE
+// and KD), from the chunk's bf16 G: dH rows = G_q W (K = V_l; split-K into fp32
+// slabs that reuse the dead logit chunk Z, so the persistent grid sees whole
+// waves), written straight to dhidden -- or, with a communicator, summed in
+// fp32 and all-reduced on the side stream while the dW GEMM runs, then cast and
+// scattered; dW (+)= G_q^T H_q (K = chunk rows).
+lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStream_t s, Header* hdr,
+                         const CUtensorMap& t_g_k, const CUtensorMap& t_w_mn, const CUtensorMap& t_g_mn,
+                         const CUtensorMap& t_h_mn, int32_t r0, float* Z, float* vdh, const int32_t* idx,
+                         uint16_t* dhidden, float* dweight, bool accumulate) {
+  const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
+  const int split = dh_split(fp, sms);
+  {
+    GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
+    float* part = split > 1 ? Z : (comm ? vdh : nullptr);
+    EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
+    LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s)));
+  }
+  if (split > 1) {
+    LaunchScope sc(LCE_K_FINAL, s);
+    reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+                                                                 dhidden, comm ? vdh : nullptr);
+    LCE_TRY(last_error());
+  }
+  if (comm) {
+    LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
+    LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
+    LCE_TRY(allreduce(comm, vdh, static_cast<size_t>(fp.Nc * fp.D), ncclSum, comm->side));
+    LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
+  }
+  {
+    GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
+    EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
+    LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s)));
+  }
+  if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
+    LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
+    LaunchScope sc(LCE_K_FINAL, s);
+    reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(vdh, 1, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+                                                                 dhidden);
+    LCE_TRY(last_error());
+  }
+  return LCE_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -895,43 +940,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
                                                                   row_grad ? gsc : nullptr, hdr, G);
       LCE_TRY(last_error());
     }
-    // S6: dH rows of the chunk = G_q W (K = V_l).  Only ceil(Nc/256) x ceil(D/256)
-    // output tiles with a very long K: split K so the persistent grid sees whole
-    // waves; fp32 partial slabs reuse the (now dead) logit chunk Z.
-    {
-      const int split = dh_split(fp, dev.sms);
-      GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
-      // vocab-parallel: the partial dH always goes through fp32 (slabs in Z, or
-      // straight into the chunk accumulator) so it can be all-reduced
-      float* part = split > 1 ? Z : (comm ? vdh : nullptr);
-      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
-      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
-      if (split > 1) {
-        LaunchScope sc(LCE_K_FINAL, s);
-        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                     dhidden, comm ? vdh : nullptr);
-        LCE_TRY(last_error());
-      }
-      if (comm) {  // S7: sum the chunk's dH over ranks on the side stream, overlapping the dW GEMM
-        LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
-        LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
-        LCE_TRY(allreduce(comm, vdh, static_cast<size_t>(fp.Nc * fp.D), ncclSum, comm->side));
-        LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
-      }
-    }
-    // S5: dW (+)= G_q^T H_q (K = chunk rows)
-    {
-      GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
-      EpiDW::Params ep{dweight, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
-      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, dev.sms, s)));
-    }
-    if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
-      LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
-      LaunchScope sc(LCE_K_FINAL, s);
-      reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(vdh, 1, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                   dhidden);
-      LCE_TRY(last_error());
-    }
+    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, t_h_mn, r0, Z, vdh, idx, dhidden,
+                        dweight, q > 0 || accumulate_dweight));
   }
   {
     LaunchScope sc(LCE_K_COMBINE, s);
@@ -1082,35 +1092,9 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
                                                                                      token_loss, idx);
       LCE_TRY(last_error());
     }
-    {  // dH_S rows of the chunk (split-K into the dead Z_S; vocab-parallel: fp32 + all-reduce), then dW_S
-      const int split = dh_split(fp, dev.sms);
-      GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
-      float* part = split > 1 ? Zs : (comm ? vdh : nullptr);
-      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden_s, idx, r0, 0, part, fp.Nc * fp.D};
-      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_ws_mn, d, ep, dev.sms, s)));
-      if (split > 1) {
-        LaunchScope sc(LCE_K_FINAL, s);
-        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Zs, split, fp.Nc * fp.D, fp.D, r0, Nc, idx,
-                                                                     hdr, dhidden_s, comm ? vdh : nullptr);
-        LCE_TRY(last_error());
-      }
-      if (comm) {
-        LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
-        LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
-        LCE_TRY(allreduce(comm, vdh, static_cast<size_t>(fp.Nc * fp.D), ncclSum, comm->side));
-        LCE_CUDA(cudaEventRecord(comm->dh_reduced, comm->side));
-      }
-      GemmDims dw{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
-      EpiDW::Params ew{dweight_s, fp.D, (q > 0 || accumulate_dweight) ? 1 : 0, hdr, 0};
-      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hs_mn, dw, ew, dev.sms, s)));
-      if (comm) {
-        LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
-        LaunchScope sc(LCE_K_FINAL, s);
-        reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(vdh, 1, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                     dhidden_s);
-        LCE_TRY(last_error());
-      }
-    }
+    // dH_S rows of the chunk and dW_S (student head only; the teacher gets no gradient)
+    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_ws_mn, t_g_mn, t_hs_mn, r0, Zs, vdh, idx, dhidden_s,
+                        dweight_s, q > 0 || accumulate_dweight));
   }
   {
     LaunchScope sc(LCE_K_COMBINE, s);
