@@ -33,7 +33,12 @@ constexpr int kGroupM = 16;  // raster: 16 m-blocks share each n-block sweep (L2
 
 constexpr int kAStageBytes = BM * BK * 2;  // 16 KB
 constexpr int kBStageBytes = BN * BK * 2;  // 32 KB
-constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*align slack*/ + 256 /*barriers*/;
+// Per epilogue warp: a 32 x 128-byte staging tile for TMA stores (4 warps).
+constexpr int kEpiWarpSmem = 4096;
+constexpr int kEpiSmemBytes = 4 * kEpiWarpSmem;
+// [A stages][B stages][barriers: 1 KB][epilogue staging] after 1 KB alignment
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*align slack*/ + 1024 /*barriers*/ +
+                           kEpiSmemBytes;
 
 // Problem extents.  M and K may live on the device (they depend on the number
 // of non-ignored tokens, which the host never reads back).
@@ -65,6 +70,7 @@ struct TileInfo {
   int row;        // row of this thread inside the tile (== TMEM lane)
   bool zero_acc;  // empty k-range: the accumulator was never written, treat as 0
   int split;      // split-K index of this work item
+  uint8_t* smem;  // this warp's 4 KB epilogue staging tile (1 KB aligned)
 };
 
 // Epilogue policies derive from EpiBase; `prefetch` runs before the epilogue
@@ -73,6 +79,9 @@ struct TileInfo {
 struct EpiBase {
   template <class P>
   static __device__ __forceinline__ void prefetch(const P&, const TileInfo&) {}
+  // after the warp's last tile (e.g. drain outstanding TMA stores)
+  template <class P>
+  static __device__ __forceinline__ void finish(const P&) {}
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -116,7 +125,7 @@ __device__ __forceinline__ WorkItem work_of(int t, int num_m, int num_n, int S, 
 template <bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmDims dims, const typename Epi::Params ep) {
+                const GemmDims dims, const __grid_constant__ typename Epi::Params ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -126,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -246,7 +256,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-      TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s};
+      TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
+                  epi_smem + q * kEpiWarpSmem};
       Epi::prefetch(ep, ti);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    Epi::finish(ep);
   }
 
   tc_fence_before();
@@ -281,12 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kPairBM = 256;  // rows per pair tile
 constexpr int kPairStages = 6;
 constexpr int kPairStageBytes = 128 * BK * 2 * 2;  // A half + B half = 32 KB
-constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 1024 + 256;
+constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 1024 + 1024 + kEpiSmemBytes;
 
 template <bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmDims dims, const typename Epi::Params ep) {
+                     const GemmDims dims, const __grid_constant__ typename Epi::Params ep) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int kHalf = 128 * BK * 2;  // 16 KB
@@ -297,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kPairStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -422,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
-                  w.kb1 == w.kb0, w.s};
+                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiWarpSmem};
       Epi::prefetch(ep, ti);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -434,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    Epi::finish(ep);
   }
 
   tc_fence_before();

@@ -42,7 +42,32 @@ struct EpiLse : EpiBase {
     int32_t row_off;      // compacted row of GEMM row 0 (row chunk of the fused path)
     float* z;             // fused path: fp32 logit chunk [rows][ldz] (cols >= n_cols: -inf), or null
     int64_t ldz;
+    int32_t use_zmap;     // 1: store the chunk through `zmap` (TMA, 32x32 fp32 boxes, 128B swizzle)
+    alignas(64) CUtensorMap zmap;
   };
+  static __device__ __forceinline__ void finish(const Params& p) {
+    if (p.use_zmap && (threadIdx.x & 31) == 0) tma_store_wait_all();
+  }
+  // One 32-column chunk of this warp's 32 rows -> Z via a TMA store: each lane
+  // writes its row's 128 bytes into the 128B-swizzled staging tile (16-byte
+  // unit v of row l at unit v ^ (l & 7)), then lane 0 issues the bulk store.
+  // Rows >= M are stored too (never read) and rows past the chunk are clipped.
+  static __device__ __forceinline__ void store_z_tma(const Params& p, const TileInfo& t, int c, const float (&x)[32]) {
+    const int l = t.row & 31;
+    if (l == 0) tma_store_wait_read();  // the previous chunk's store has consumed the staging tile
+    __syncwarp();
+    uint8_t* st = t.smem;
+#pragma unroll
+    for (int v = 0; v < 8; ++v)
+      *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
+          make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+    fence_async_smem();
+    __syncwarp();
+    if (l == 0) {
+      tma_store_2d(&p.zmap, st, t.n0 + c * 32, t.m0 + (t.row - l));
+      tma_store_commit();
+    }
+  }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
@@ -59,7 +84,9 @@ struct EpiLse : EpiBase {
         for (int j = 0; j < 32; ++j)
           if (cb + j >= p.n_cols) x[j] = -INFINITY;
       }
-      if (zrow) {
+      if (p.use_zmap) {
+        store_z_tma(p, t, c, x);
+      } else if (zrow) {
 #pragma unroll
         for (int v = 0; v < 8; ++v) zrow[c * 8 + v] = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
       }

@@ -297,6 +297,21 @@ lce_status_t encode_map(CUtensorMap* m, const void* base, int64_t inner, int64_t
   return LCE_OK;
 }
 
+// fp32 row-major [rows, inner] (pitch `pitch` floats) for TMA stores of
+// 32 x 32 boxes (128-byte inner extent, 128-byte swizzle).
+lce_status_t map_f32_store(CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int64_t pitch) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return LCE_ERR_CUDA;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch * 4)};
+  cuuint32_t box[2] = {32u, 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? LCE_OK : LCE_ERR_CUDA;
+}
+
 // K-major operand stored [rows, K]: box {64 of K, box_rows}.
 lce_status_t map_kmajor(CUtensorMap* m, const void* base, int64_t rows, int64_t K, int64_t pitch, int box_rows) {
   return encode_map(m, base, K, rows, pitch, box_rows);
@@ -363,6 +378,14 @@ bool use_pair() {
   const char* e = getenv("LCE_GEMM");
   return !(e && strcmp(e, "single") == 0);
 }
+// Fused path: the fp32 logit chunk leaves the forward epilogue through TMA
+// stores (128B-swizzled 32x32 staging tiles) instead of per-thread row stores;
+// LCE_ZSTORE=direct selects the st.global path (A/B comparisons).
+int z_tma() {
+  const char* e = getenv("LCE_ZSTORE");
+  return (e && strcmp(e, "direct") == 0) ? 0 : 1;
+}
+
 // Rows of the TMA box of a K-major B operand: each CTA of a pair stages half of
 // the 256-column tile.
 int b_box_rows() { return use_pair() ? BN / 2 : BN; }
@@ -902,6 +925,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
       EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, Z, fp.ldv};
+      ep.use_zmap = z_tma();
+      if (ep.use_zmap) LCE_TRY(map_f32_store(&ep.zmap, Z, fp.ldv, fp.Nc, fp.ldv));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
     const unsigned cb = static_cast<unsigned>(fp.Nc / kRowsPerCta);
@@ -1047,9 +1072,13 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
       GemmDims ds{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
       const int32_t voff = static_cast<int32_t>(p->vocab_start);
       EpiLse::Params es{yc, voff, Vl, pms, pss, fp.Nc, zt, r0, Zs, fp.ldv};
+      es.use_zmap = z_tma();
+      if (es.use_zmap) LCE_TRY(map_f32_store(&es.zmap, Zs, fp.ldv, fp.Nc, fp.ldv));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_hs_k, t_ws_k, ds, es, dev.sms, s)));
       GemmDims dt{&hdr->n_valid, 0, nullptr, Dt, Vl, r0, Nc, 0, 0};
       EpiLse::Params et{yc, voff, Vl, pmt, pst, fp.Nc, zt, r0, Zt, fp.ldv};
+      et.use_zmap = z_tma();
+      if (et.use_zmap) LCE_TRY(map_f32_store(&et.zmap, Zt, fp.ldv, fp.Nc, fp.ldv));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_ht_k, t_wt_k, dt, et, dev.sms, s)));
     }
     const unsigned cb = static_cast<unsigned>(fp.Nc / kRowsPerCta);
