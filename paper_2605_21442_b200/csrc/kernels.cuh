@@ -136,28 +136,65 @@ struct EpiG : EpiBase {
     uint16_t* G;          // [rows_cap][ldg] bf16
     int64_t ldg;
     const float* row_scale;  // [N_v] per-token upstream gradient (reduction NONE) or null
+    int32_t use_gmap;        // 1: store through `gmap` (TMA, 64-col x 32-row bf16 boxes, 128B swizzle)
+    alignas(64) CUtensorMap gmap;
   };
+  static __device__ __forceinline__ void finish(const Params& p) {
+    if (p.use_gmap && (threadIdx.x & 31) == 0) tma_store_wait_all();
+  }
+  // G of one 32-column chunk of this thread's row, as 16 packed bf16 pairs.
+  static __device__ __forceinline__ void g_chunk(const Params& p, uint32_t taddr, const TileInfo& t, int c,
+                                                 bool valid, int yl, float lsel, float rs, uint32_t* w) {
+    float x[32];
+    load_chunk(taddr, c, t.zero_acc, x);
+    const int cb = t.n0 + c * 32;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c * 32 + j == yl ? 1.f : 0.f);
+      float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c * 32 + j + 1 == yl ? 1.f : 0.f);
+      g0 = (!valid || cb + j >= p.n_cols) ? 0.f : g0 * rs;
+      g1 = (!valid || cb + j + 1 >= p.n_cols) ? 0.f : g1 * rs;
+      w[j / 2] = pack_bf16x2(g0, g1);
+    }
+  }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;
     const float lsel = valid ? p.lse_c[r] * kLog2e : 0.f;
     const float rs = (valid && p.row_scale) ? p.row_scale[r] : 1.f;
+    if (p.use_gmap) {
+      // Two chunks (64 bf16 = 128 bytes per row) per TMA store: each lane
+      // writes its row into the 128B-swizzled staging tile (16-byte unit v of
+      // row l at unit v ^ (l & 7)), lane 0 issues the store.  Rows >= M are
+      // stored as zeros; rows/columns past the buffer are clipped by TMA.
+      const int l = t.row & 31;
+#pragma unroll 1
+      for (int c2 = 0; c2 < BN / 64; ++c2) {
+        uint32_t w[32];
+        g_chunk(p, taddr, t, 2 * c2, valid, yl, lsel, rs, w);
+        g_chunk(p, taddr, t, 2 * c2 + 1, valid, yl, lsel, rs, w + 16);
+        if (l == 0) tma_store_wait_read();
+        __syncwarp();
+        uint8_t* st = t.smem;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<uint4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
+              make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (l == 0) {
+          tma_store_2d(&p.gmap, st, t.n0 + c2 * 64, t.m0 + (t.row - l));
+          tma_store_commit();
+        }
+      }
+      return;
+    }
     uint4* dst = reinterpret_cast<uint4*>(p.G + static_cast<int64_t>(r) * p.ldg + t.n0);
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
-      float x[32];
-      load_chunk(taddr, c, t.zero_acc, x);
-      const int cb = t.n0 + c * 32;
       uint32_t w[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c * 32 + j == yl ? 1.f : 0.f);
-        float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c * 32 + j + 1 == yl ? 1.f : 0.f);
-        g0 = (!valid || cb + j >= p.n_cols) ? 0.f : g0 * rs;
-        g1 = (!valid || cb + j + 1 >= p.n_cols) ? 0.f : g1 * rs;
-        w[j / 2] = pack_bf16x2(g0, g1);
-      }
+      g_chunk(p, taddr, t, c, valid, yl, lsel, rs, w);
 #pragma unroll
       for (int v = 0; v < 4; ++v) dst[c * 4 + v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
     }
@@ -328,33 +365,56 @@ struct EpiAdamW : EpiBase {
       float x[32];
       load_chunk(taddr, c, t.zero_acc, x);
       const int cb = t.n0 + c * 32;
-      if (!valid) continue;
+      if (!valid || cb >= t.N) continue;
+      if (cb + 32 <= t.N) {
+        // whole chunk in range: issue all 24 loads before any arithmetic so
+        // the row's three 128-byte segments are in flight together
+        float4 th[8], m[8], s[8];
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int col = cb + 4 * v;
-        if (col >= t.N) break;
-        float4 th = *reinterpret_cast<const float4*>(p.theta + rowoff + col);
-        float4 m = *reinterpret_cast<const float4*>(p.exp_avg + rowoff + col);
-        float4 s = *reinterpret_cast<const float4*>(p.exp_avg_sq + rowoff + col);
-        float* thv = &th.x;
-        float* mv = &m.x;
-        float* sv = &s.x;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float g = cs * x[4 * v + e];
-          thv[e] = thv[e] * p.decay;
-          mv[e] = mv[e] + (1.f - p.beta1) * (g - mv[e]);  // torch: exp_avg.lerp_(grad, 1 - beta1)
-          sv[e] = p.beta2 * sv[e] + (1.f - p.beta2) * g * g;
-          const float denom = __fdiv_rn(__fsqrt_rn(sv[e]), p.sqrt_bc2) + p.eps;
-          thv[e] = thv[e] - p.step_size * __fdiv_rn(mv[e], denom);
+        for (int v = 0; v < 8; ++v) {
+          th[v] = *reinterpret_cast<const float4*>(p.theta + rowoff + cb + 4 * v);
+          m[v] = *reinterpret_cast<const float4*>(p.exp_avg + rowoff + cb + 4 * v);
+          s[v] = *reinterpret_cast<const float4*>(p.exp_avg_sq + rowoff + cb + 4 * v);
         }
-        *reinterpret_cast<float4*>(p.theta + rowoff + col) = th;
-        *reinterpret_cast<float4*>(p.exp_avg + rowoff + col) = m;
-        *reinterpret_cast<float4*>(p.exp_avg_sq + rowoff + col) = s;
-        *reinterpret_cast<uint2*>(p.w + rowoff + col) =
-            make_uint2(pack_bf16x2(th.x, th.y), pack_bf16x2(th.z, th.w));
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          step4(p, cs, x + 4 * v, th[v], m[v], s[v]);
+          store4(p, rowoff + cb + 4 * v, th[v], m[v], s[v]);
+        }
+      } else {
+        for (int v = 0; v < 8 && cb + 4 * v < t.N; ++v) {
+          const int64_t o = rowoff + cb + 4 * v;
+          float4 th = *reinterpret_cast<const float4*>(p.theta + o);
+          float4 m = *reinterpret_cast<const float4*>(p.exp_avg + o);
+          float4 s = *reinterpret_cast<const float4*>(p.exp_avg_sq + o);
+          step4(p, cs, x + 4 * v, th, m, s);
+          store4(p, o, th, m, s);
+        }
       }
     }
+  }
+  // torch.optim.AdamW's single-tensor update order (R22) on 4 elements
+  static __device__ __forceinline__ void step4(const Params& p, float cs, const float* x, float4& th, float4& m,
+                                               float4& s) {
+    float* thv = &th.x;
+    float* mv = &m.x;
+    float* sv = &s.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float g = cs * x[e];
+      thv[e] = thv[e] * p.decay;
+      mv[e] = mv[e] + (1.f - p.beta1) * (g - mv[e]);  // torch: exp_avg.lerp_(grad, 1 - beta1)
+      sv[e] = p.beta2 * sv[e] + (1.f - p.beta2) * g * g;
+      const float denom = __fdiv_rn(__fsqrt_rn(sv[e]), p.sqrt_bc2) + p.eps;
+      thv[e] = thv[e] - p.step_size * __fdiv_rn(mv[e], denom);
+    }
+  }
+  static __device__ __forceinline__ void store4(const Params& p, int64_t o, const float4& th, const float4& m,
+                                                const float4& s) {
+    *reinterpret_cast<float4*>(p.theta + o) = th;
+    *reinterpret_cast<float4*>(p.exp_avg + o) = m;
+    *reinterpret_cast<float4*>(p.exp_avg_sq + o) = s;
+    *reinterpret_cast<uint2*>(p.w + o) = make_uint2(pack_bf16x2(th.x, th.y), pack_bf16x2(th.z, th.w));
   }
 };
 

@@ -380,7 +380,8 @@ bool use_pair() {
 }
 // Fused path: the fp32 logit chunk leaves the forward epilogue through TMA
 // stores (128B-swizzled 32x32 staging tiles) instead of per-thread row stores;
-// LCE_ZSTORE=direct selects the st.global path (A/B comparisons).
+// the split path's bf16 G chunk likewise (64x32 boxes).  LCE_ZSTORE=direct
+// selects the st.global path for both (A/B comparisons).
 int z_tma() {
   const char* e = getenv("LCE_ZSTORE");
   return (e && strcmp(e, "direct") == 0) ? 0 : 1;
@@ -729,6 +730,8 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(pl.D), static_cast<int32_t>(vc)};
       EpiG::Params ep{yc, lsec, static_cast<int32_t>(p->vocab_start + v0), static_cast<int32_t>(vc), G, pl.Vc,
                       row_grad ? gsc : nullptr};
+      ep.use_gmap = z_tma();
+      if (ep.use_gmap) LCE_TRY(encode_map(&ep.gmap, G, pl.Vc, pl.cap, pl.Vc, 32));
       LCE_TRY((launch_gemm<false, false, EpiG>(LCE_K_BWD_G, t_hc_k, t_w_k, d, ep, dev.sms, s)));
     }
     // S6: dH (+)= G_c W_c   (A = G_c K-major over vocab, B = W_c MN-major)

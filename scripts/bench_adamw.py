@@ -37,6 +37,16 @@ def timed(fn, steps, warmup=2):
     return a.elapsed_time(b) / steps, torch.cuda.max_memory_allocated()
 
 
+def breakdown(fn):
+    """Per-kernel-class device ms of one step (CUDA events around each launch)."""
+    F.profile_read()
+    F.profile_enable(True)
+    fn()
+    torch.cuda.synchronize()
+    F.profile_enable(False)
+    return {k: round(ms, 3) for k, (ms, n) in F.profile_read().items() if n}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="llama8b")
@@ -61,6 +71,7 @@ def main():
         W.copy_(master.detach())
 
     res["separate"] = timed(step_a, args.steps)
+    prof = {"separate": breakdown(step_a)}
     del opt, master, dW
     torch.cuda.empty_cache()
 
@@ -77,7 +88,8 @@ def main():
         F.backward_adamw(H, W2, y, out["lse"], theta, m, v, lr=1e-5, weight_decay=0.01, step=count[0], workspace=ws)
 
     res["in_backward"] = timed(step_b, args.steps)
-    print(json.dumps({k: {"ms_per_step": round(t, 3), "peak_hbm_gb": round(mem / 1e9, 2)}
+    prof["in_backward"] = breakdown(step_b)
+    print(json.dumps({k: {"ms_per_step": round(t, 3), "peak_hbm_gb": round(mem / 1e9, 2), "kernels_ms": prof[k]}
                       for k, (t, mem) in res.items()}))
 
 
