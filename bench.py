@@ -183,7 +183,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk-budget", type=int, default=0,
-                    help="chunk_budget_bytes (fused: logit+G chunk bytes, default 4 GiB; split: G chunk, 512 MiB)")
+                    help="chunk_budget_bytes (fused: bf16 q/G chunk bytes, default 2 GiB; split: G chunk, 512 MiB)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "split"],
                     help="fused = lce_forward_backward (no logit recompute, 6 N_v V D flops); split = "
                          "lce_forward + lce_backward (recompute from lse, 8 N_v V D flops); auto = fused")

@@ -159,13 +159,14 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
  * The same results as lce_forward followed by lce_backward (loss, lse,
  * token_loss, n_valid, dhidden, dweight; same argument meanings), computed
  * without recomputing the logits: P:166's "processes hidden states in
- * chunks" taken literally -- for each chunk of Nc compacted rows the fp32
- * logits z = H_c W^T are kept (in the workspace, Nc x V_l x 4 bytes, never
- * N x V_l), reduced to lse, turned into G in place and consumed by the dH and
- * dW GEMMs: 6 N_v V D flops instead of 8.  The upstream gradient must be
- * known up front (grad_loss as in lce_backward; NULL = 1).  dW is accumulated
- * across row chunks in fp32.  Nc is set by chunk_budget_bytes (bytes of the
- * fp32 + bf16 chunk buffers; 0 = 4 GiB).  With comm != NULL (vocab-parallel,
+ * chunks" taken literally -- for each chunk of Nc compacted rows the
+ * forward epilogue keeps q = exp(z - m_tile) in bf16 (z = H_c W^T in fp32,
+ * m_tile the row max over its 256-column tile; in the workspace, Nc x V_l x 2
+ * bytes, never N x V_l), the rows are reduced to lse, q is turned into G in
+ * place and consumed by the dH and dW GEMMs: 6 N_v V D flops instead of 8.
+ * The upstream gradient must be known up front (grad_loss as in lce_backward;
+ * NULL = 1).  dW is accumulated across row chunks in fp32.  Nc is set by
+ * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB).  With comm != NULL (vocab-parallel,
  * P:180) each row chunk's (max, sum-exp, target logit) are combined with the
  * same MAX / SUM all-reduces as lce_forward, and the chunk's fp32 dH partial is
  * all-reduced on the communicator's side stream while the dW GEMM runs. */

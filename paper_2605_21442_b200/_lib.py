@@ -10,7 +10,9 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblce.so")
+# LCE_LIB_PATH: load another build of the same library (A/B timing of two
+# revisions on one box); the default is the in-tree build.
+LIB_PATH = os.environ.get("LCE_LIB_PATH") or os.path.join(_PKG, "liblce.so")
 
 LCE_K_COUNT = 9
 KERNEL_CLASSES = ["prep", "gather", "fwd_gemm", "combine", "bwd_g", "bwd_dh", "bwd_dw", "finalize", "comm"]

@@ -25,11 +25,18 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // ============================================================ S1+S2 forward epilogue
-// Per row of the 128x256 logit tile (still in TMEM): running max m and
-// sum-exp s relative to m over the tile's valid columns (cols >= n_cols are
-// -inf), and the target logit if the row's label falls in this tile.
-// Writes the partials (m, s) of tile column n_blk; the logits never leave
-// the SM.  (the dense [B,S,V] tensor is never materialised.)
+// Per row of the 128x256 logit tile (still in TMEM), two passes over the fp32
+// accumulator: pass 1 takes the row max m over the tile's valid columns (cols
+// >= n_cols are -inf) and the target logit if the row's label falls in this
+// tile; pass 2 sums e = exp(z - m) in fp32.  Writes the partials (m, s) of
+// tile column n_blk; the logits never leave the SM (the dense [B,S,V]
+// tensor is never materialised).  Every path uses the same passes and the
+// same summation order, so lse is bitwise identical across them.
+//   fused CE path (store_q): pass 2 also stores e rounded to bf16 (q, in
+//     [0, 1]; 2 bytes per logit) so the G fix-up can rescale it by
+//     exp(m - lse) (R24).  Logits are never rounded (R8): only the
+//     probabilities relative to the tile max are.
+//   KD path (use_zmap / z): pass 1 stores the fp32 logits.
 struct EpiLse : EpiBase {
   struct Params {
     const int32_t* yc;    // [N_v] compacted labels (global vocab ids)
@@ -40,40 +47,70 @@ struct EpiLse : EpiBase {
     int64_t ld;
     float* zt;            // [N_v] target logit (single writer: the owning tile)
     int32_t row_off;      // compacted row of GEMM row 0 (row chunk of the fused path)
-    float* z;             // fused path: fp32 logit chunk [rows][ldz] (cols >= n_cols: -inf), or null
+    float* z;             // KD path: fp32 logit chunk [rows][ldz] (cols >= n_cols: -inf), or null
     int64_t ldz;
-    int32_t use_zmap;     // 1: store the chunk through `zmap` (TMA, 32x32 fp32 boxes, 128B swizzle)
+    int32_t use_zmap;     // 1: store the fp32 chunk through `zmap` (TMA, 32x32 fp32 boxes, 128B swizzle)
+    int32_t store_q;      // 1 (fused CE): store q = exp(z - m_tile) in bf16 through `zmap` (64x32 boxes)
     alignas(64) CUtensorMap zmap;
   };
   static __device__ __forceinline__ void finish(const Params& p) {
-    if (p.use_zmap && (threadIdx.x & 31) == 0) tma_store_wait_all();
+    if ((p.use_zmap || p.store_q) && (threadIdx.x & 31) == 0) tma_store_wait_all();
   }
-  // One 32-column chunk of this warp's 32 rows -> Z via a TMA store: each lane
-  // writes its row's 128 bytes into the 128B-swizzled staging tile (16-byte
-  // unit v of row l at unit v ^ (l & 7)), then lane 0 issues the bulk store.
-  // Rows >= M are stored too (never read) and rows past the chunk are clipped.
-  static __device__ __forceinline__ void store_z_tma(const Params& p, const TileInfo& t, int c, const float (&x)[32]) {
+  // Stage this warp's 32 rows x 128 bytes in the 128B-swizzled tile (16-byte
+  // unit v of row l at unit v ^ (l & 7)) and let lane 0 issue the TMA store
+  // at (col, row0).  Rows >= M are stored too (never read); rows past the
+  // buffer are clipped.
+  static __device__ __forceinline__ void tma_rows(const Params& p, const TileInfo& t, int col, const uint4 (&u)[8]) {
     const int l = t.row & 31;
-    if (l == 0) tma_store_wait_read();  // the previous chunk's store has consumed the staging tile
+    if (l == 0) tma_store_wait_read();  // the previous store has consumed the staging tile
     __syncwarp();
     uint8_t* st = t.smem;
 #pragma unroll
-    for (int v = 0; v < 8; ++v)
-      *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
-          make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+    for (int v = 0; v < 8; ++v) *reinterpret_cast<uint4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) = u[v];
     fence_async_smem();
     __syncwarp();
     if (l == 0) {
-      tma_store_2d(&p.zmap, st, t.n0 + c * 32, t.m0 + (t.row - l));
+      tma_store_2d(&p.zmap, st, col, t.m0 + (t.row - l));
       tma_store_commit();
     }
+  }
+  template <bool kStoreQ>
+  static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, const TileInfo& t, float ml) {
+    float s = 0.f;
+#pragma unroll 1
+    for (int c2 = 0; c2 < BN / 64; ++c2) {
+      uint32_t w[32];
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float x[32];
+        load_chunk(taddr, 2 * c2 + h, t.zero_acc, x);
+        const int cb = t.n0 + (2 * c2 + h) * 32;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float e0 = cb + j < p.n_cols ? ex2_approx(fmaf(x[j], kLog2e, -ml)) : 0.f;
+          const float e1 = cb + j + 1 < p.n_cols ? ex2_approx(fmaf(x[j + 1], kLog2e, -ml)) : 0.f;
+          a0 += e0;
+          a1 += e1;
+          if (kStoreQ) w[h * 16 + j / 2] = pack_bf16x2(e0, e1);
+        }
+      }
+      s += a0 + a1;
+      if (kStoreQ) {
+        uint4 u[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) u[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+        tma_rows(p, t, t.n0 + c2 * 64, u);
+      }
+    }
+    return s;
   }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[p.row_off + r] - p.label_off - t.n0) : -1;  // tile-relative target column
-    float m = -INFINITY, s = 0.f, zt = 0.f;
     float4* zrow = (p.z && valid) ? reinterpret_cast<float4*>(p.z + static_cast<int64_t>(r) * p.ldz + t.n0) : nullptr;
+    float m = -INFINITY, zt = 0.f;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float x[32];
@@ -85,7 +122,12 @@ struct EpiLse : EpiBase {
           if (cb + j >= p.n_cols) x[j] = -INFINITY;
       }
       if (p.use_zmap) {
-        store_z_tma(p, t, c, x);
+        uint4 u[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          u[v] = make_uint4(__float_as_uint(x[4 * v]), __float_as_uint(x[4 * v + 1]), __float_as_uint(x[4 * v + 2]),
+                            __float_as_uint(x[4 * v + 3]));
+        tma_rows(p, t, t.n0 + c * 32, u);
       } else if (zrow) {
 #pragma unroll
         for (int v = 0; v < 8; ++v) zrow[c * 8 + v] = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
@@ -96,24 +138,11 @@ struct EpiLse : EpiBase {
         for (int j = 0; j < 32; ++j)
           if (j == jt) zt = x[j];
       }
-      float cm = x[0];
 #pragma unroll
-      for (int j = 1; j < 32; ++j) cm = fmaxf(cm, x[j]);
-      const float mn = fmaxf(m, cm);
-      if (mn == -INFINITY) continue;  // whole chunk masked and nothing before it
-      const float mnl = mn * kLog2e;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        a0 += ex2_approx(fmaf(x[j + 0], kLog2e, -mnl));
-        a1 += ex2_approx(fmaf(x[j + 1], kLog2e, -mnl));
-        a2 += ex2_approx(fmaf(x[j + 2], kLog2e, -mnl));
-        a3 += ex2_approx(fmaf(x[j + 3], kLog2e, -mnl));
-      }
-      const float cs = (a0 + a1) + (a2 + a3);
-      s = (m == -INFINITY) ? cs : fmaf(s, ex2_approx((m - mn) * kLog2e), cs);
-      m = mn;
+      for (int j = 0; j < 32; ++j) m = fmaxf(m, x[j]);
     }
+    const float ml = (m == -INFINITY) ? 0.f : m * kLog2e;
+    const float s = p.store_q ? sum_exp<true>(p, taddr, t, ml) : sum_exp<false>(p, taddr, t, ml);
     if (valid) {
       p.part_m[t.n_blk * p.ld + r] = m;
       p.part_s[t.n_blk * p.ld + r] = s;
@@ -769,43 +798,56 @@ __global__ void __launch_bounds__(256) combine_chunk_vp_kernel(int mode, const f
   if (ltok) ltok[r] = l;
 }
 
-// S4 of the fused path without the recompute: the chunk's fp32 logits Z (kept
-// from the forward GEMM) -> G = s_i (exp(z - lse_i) - [j == y_i]) in bf16,
-// s_i = c (MEAN / SUM) or g_i (NONE); rows in [M, ceil64(M)) and columns
-// >= n_cols are zero.  One CTA per row, 8 columns per thread per step.
-__global__ void __launch_bounds__(256) fixup_g_kernel(const float* __restrict__ Z, int64_t ldz, int n_cols,
-                                                      int row_off, int cap, const int32_t* __restrict__ yc,
-                                                      int32_t label_off, const float* __restrict__ lse_c,
+// S4 of the fused CE path, in place: q = exp(z - m_t) (bf16, stored by the
+// forward epilogue relative to the max m_t of its 256-column tile t) ->
+// G = s_i (q exp(m_t - lse_i) - [j == y_i]) in bf16.  The target column is
+// formed from the fp32 target logit instead, s_i (exp(z_y - lse_i) - 1), so
+// the cancellation near p = 1 keeps its fp32 accuracy.  Rows in
+// [M, ceil64(M)) and columns >= n_cols become zero.  One CTA per row.
+__global__ void __launch_bounds__(256) fixup_q_kernel(uint16_t* __restrict__ Q, int64_t ldq, int n_cols, int row_off,
+                                                      int cap, const int32_t* __restrict__ yc, int32_t label_off,
+                                                      const float* __restrict__ lse_c,
                                                       const float* __restrict__ row_scale, const Header* hdr,
-                                                      uint16_t* __restrict__ G) {
+                                                      const float* __restrict__ pm, int64_t ld_pm,
+                                                      const float* __restrict__ zt) {
   const int m = blockIdx.x;
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= ((M + 63) & ~63)) return;
-  uint4* grow = reinterpret_cast<uint4*>(G + static_cast<int64_t>(m) * ldz);
-  const int nvec = static_cast<int>(ldz / 8);
+  uint4* qrow = reinterpret_cast<uint4*>(Q + static_cast<int64_t>(m) * ldq);
+  const int nvec = static_cast<int>(ldq / 8);
   if (m >= M) {
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) grow[v] = make_uint4(0, 0, 0, 0);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) qrow[v] = make_uint4(0, 0, 0, 0);
     return;
   }
   const int r = row_off + m;
-  const float lsel = lse_c[r] * kLog2e;
+  const float lse = lse_c[r];
   const int yl = yc[r] - label_off;
   const float sc = hdr->c * (row_scale ? row_scale[r] : 1.f);
-  const float4* zrow = reinterpret_cast<const float4*>(Z + static_cast<int64_t>(m) * ldz);
   for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
-    const float4 a = zrow[2 * v], b = zrow[2 * v + 1];
-    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const int c0 = 8 * v;
+    const float a = sc * ex2_approx((pm[static_cast<int64_t>(c0 / BN) * ld_pm + m] - lse) * kLog2e);
+    const uint4 in = qrow[v];
+    const uint32_t wi[4] = {in.x, in.y, in.z, in.w};
     uint32_t w[4];
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const int c0 = 8 * v + j;
-      float g0 = ex2_approx(fmaf(x[j], kLog2e, -lsel)) - (c0 == yl ? 1.f : 0.f);
-      float g1 = ex2_approx(fmaf(x[j + 1], kLog2e, -lsel)) - (c0 + 1 == yl ? 1.f : 0.f);
-      g0 = c0 < n_cols ? g0 * sc : 0.f;
-      g1 = c0 + 1 < n_cols ? g1 * sc : 0.f;
-      w[j / 2] = pack_bf16x2(g0, g1);
+    for (int j = 0; j < 4; ++j) {
+      const float2 e = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wi[j]));
+      const int c = c0 + 2 * j;
+      const float g0 = c < n_cols ? a * e.x : 0.f;
+      const float g1 = c + 1 < n_cols ? a * e.y : 0.f;
+      w[j] = pack_bf16x2(g0, g1);
     }
-    grow[v] = make_uint4(w[0], w[1], w[2], w[3]);
+    if (yl >= c0 && yl < c0 + 8 && yl < n_cols) {
+      const float gt = sc * (ex2_approx((zt[r] - lse) * kLog2e) - 1.f);
+      const int j = (yl - c0) >> 1;
+      __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w[j]);
+      if ((yl - c0) & 1)
+        h.y = __float2bfloat16_rn(gt);
+      else
+        h.x = __float2bfloat16_rn(gt);
+      w[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    qrow[v] = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 

@@ -102,18 +102,47 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
 }
 
 // Fused fwd+bwd (lce_forward_backward): row chunks of Nc compacted tokens keep
-// their fp32 logits Z [Nc, ldv] and bf16 G [Nc, ldv]; 6 bytes per element are
-// bounded by the budget (default 4 GiB), never N x V_l.
-constexpr int64_t kDefaultFusedBudget = 4ll << 30;
+// q = exp(z - m_tile) in bf16 [Nc, ldv], turned into G in place (R24): 2 bytes
+// per element bounded by the budget (default 2 GiB), never N x V_l.  The KD
+// path keeps fp32 logits for student and teacher (see KdPlan).
+constexpr int64_t kDefaultFusedBudget = 2ll << 30;
+constexpr int64_t kDefaultKdBudget = 4ll << 30;
+constexpr int kPlanSms = 148;  // B200: the split-K choice is made at plan time (host-pure sizes)
 
 struct FusedPlan {
   int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
-  size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g;
+  int split;                       // split-K factor of the chunk's dH GEMM
+  size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, slab;
   size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
   size_t total;
 };
 
-bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
+int use_pair_units(int sms);
+
+// Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
+// work items fill the persistent grid's last wave to >= 97% (else the best).
+// `max_split` bounds it where the fp32 slabs alias another buffer.
+int dh_split(int64_t Nc, int64_t D, int max_split, int sms) {
+  const int64_t units = use_pair_units(sms);
+  const int64_t rows = units == sms ? 128 : 256;
+  const int64_t tiles = ceil_div(Nc, rows) * ceil_div(D, BN);
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 8 && s <= max_split; ++s) {
+    const int64_t items = tiles * s;
+    const double eff = static_cast<double>(items) / (ceil_div(items, units) * units);
+    if (eff > best_eff + 1e-9) {
+      best = s;
+      best_eff = eff;
+    }
+    if (eff >= 0.97) break;
+  }
+  return best;
+}
+
+// kd: student chunk keeps fp32 Z + bf16 G (6 bytes per element), the dH
+// split-K slabs alias Z; otherwise the CE layout above with its own slabs.
+bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   Plan base;
   if (!make_plan(p, &base)) return false;
   FusedPlan q{};
@@ -123,12 +152,14 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
   q.cap = base.cap;
   q.ldv = round_up(q.Vl, BN);
   q.n_tiles = ceil_div(q.Vl, BN);
+  const int64_t per_elem = kd ? 6 : 2;
   const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
-  int64_t nc_max = (budget / (6 * q.ldv)) / kPairBM * kPairBM;
+  int64_t nc_max = (budget / (per_elem * q.ldv)) / kPairBM * kPairBM;
   if (nc_max < kPairBM) nc_max = kPairBM;
   if (nc_max > q.cap) nc_max = q.cap;
   q.n_chunks = ceil_div(q.cap, nc_max);
   q.Nc = round_up(ceil_div(q.cap, q.n_chunks), kPairBM);  // balanced chunks
+  q.split = dh_split(q.Nc, q.D, kd ? static_cast<int>(q.ldv / q.D) : 8, kPlanSms);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -145,8 +176,9 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp) {
   q.hc = take(static_cast<size_t>((q.n_chunks * q.Nc) * q.D * 2));
   q.pm = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
   q.ps = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
-  q.z = take(static_cast<size_t>(q.Nc * q.ldv * 4));
+  q.z = kd ? take(static_cast<size_t>(q.Nc * q.ldv * 4)) : 0;
   q.g = take(static_cast<size_t>(q.Nc * q.ldv * 2));
+  q.slab = kd ? q.z : take(q.split > 1 ? static_cast<size_t>(q.split * q.Nc * q.D * 4) : 0);
   q.vmloc = take(static_cast<size_t>(q.Nc * 4));
   q.vmglob = take(static_cast<size_t>(q.Nc * 4));
   q.vsz = take(static_cast<size_t>(q.Nc * 8));
@@ -168,10 +200,10 @@ bool make_kd_plan(const lce_problem_t* p, int64_t teacher_dim, KdPlan* kp) {
   if (teacher_dim <= 0 || teacher_dim % 8 != 0 || teacher_dim >= (1ll << 31)) return false;
   lce_problem_t q = *p;
   // the student plan sized for 10 bytes per element instead of 6
-  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
+  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultKdBudget;
   q.chunk_budget_bytes = budget * 6 / 10;
   KdPlan k{};
-  if (!make_fused_plan(&q, &k.f)) return false;
+  if (!make_fused_plan(&q, &k.f, true)) return false;
   k.Dt = teacher_dim;
   size_t off = k.f.total;
   auto take = [&](size_t bytes) {
@@ -187,29 +219,6 @@ bool make_kd_plan(const lce_problem_t* p, int64_t teacher_dim, KdPlan* kp) {
   k.total = off;
   *kp = k;
   return true;
-}
-
-bool use_pair();
-
-// Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
-// work items fill the persistent grid's last wave to >= 97% (else the best),
-// with the fp32 slabs fitting in the logit chunk buffer (split * D <= ldv).
-int dh_split(const FusedPlan& fp, int sms) {
-  const int64_t units = use_pair() ? sms / 2 : sms;
-  const int64_t rows = use_pair() ? 256 : 128;
-  const int64_t tiles = ceil_div(fp.Nc, rows) * ceil_div(fp.D, BN);
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 8 && s * fp.D <= fp.ldv; ++s) {
-    const int64_t items = tiles * s;
-    const double eff = static_cast<double>(items) / (ceil_div(items, units) * units);
-    if (eff > best_eff + 1e-9) {
-      best = s;
-      best_eff = eff;
-    }
-    if (eff >= 0.97) break;
-  }
-  return best;
 }
 
 // ------------------------------------------------------------------ device / driver
@@ -378,6 +387,8 @@ bool use_pair() {
   const char* e = getenv("LCE_GEMM");
   return !(e && strcmp(e, "single") == 0);
 }
+// persistent work units of the GEMM grid: CTA pairs, or single CTAs
+int use_pair_units(int sms) { return use_pair() ? sms / 2 : sms; }
 // Fused path: the fp32 logit chunk leaves the forward epilogue through TMA
 // stores (128B-swizzled 32x32 staging tiles) instead of per-thread row stores;
 // the split path's bf16 G chunk likewise (64x32 boxes).  LCE_ZSTORE=direct
@@ -785,19 +796,19 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
 // scattered; dW (+)= G_q^T H_q (K = chunk rows).
 lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStream_t s, Header* hdr,
                          const CUtensorMap& t_g_k, const CUtensorMap& t_w_mn, const CUtensorMap& t_g_mn,
-                         const CUtensorMap& t_h_mn, int32_t r0, float* Z, float* vdh, const int32_t* idx,
+                         const CUtensorMap& t_h_mn, int32_t r0, float* slab, float* vdh, const int32_t* idx,
                          uint16_t* dhidden, float* dweight, bool accumulate) {
   const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
-  const int split = dh_split(fp, sms);
+  const int split = fp.split;
   {
     GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
-    float* part = split > 1 ? Z : (comm ? vdh : nullptr);
+    float* part = split > 1 ? slab : (comm ? vdh : nullptr);
     EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
     LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s)));
   }
   if (split > 1) {
     LaunchScope sc(LCE_K_FINAL, s);
-    reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
+    reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(slab, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
                                                                  dhidden, comm ? vdh : nullptr);
     LCE_TRY(last_error());
   }
@@ -891,8 +902,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
   uint16_t* hc = reinterpret_cast<uint16_t*>(ws + fp.hc);
   float* pm = reinterpret_cast<float*>(ws + fp.pm);
   float* ps = reinterpret_cast<float*>(ws + fp.ps);
-  float* Z = reinterpret_cast<float*>(ws + fp.z);
-  uint16_t* G = reinterpret_cast<uint16_t*>(ws + fp.g);
+  uint16_t* G = reinterpret_cast<uint16_t*>(ws + fp.g);  // q of the chunk, then G in place
+  float* slab = reinterpret_cast<float*>(ws + fp.slab);
   float* vmloc = reinterpret_cast<float*>(ws + fp.vmloc);
   float* vmglob = reinterpret_cast<float*>(ws + fp.vmglob);
   float* vsz = reinterpret_cast<float*>(ws + fp.vsz);
@@ -924,12 +935,12 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
     CUtensorMap t_h_k, t_h_mn;
     LCE_TRY(map_kmajor(&t_h_k, hq, fp.Nc, fp.D, fp.D, BM));
     LCE_TRY(map_mnmajor(&t_h_mn, hq, fp.Nc, fp.D, fp.D));
-    // S1+S2 (+ keep the fp32 logit chunk): z = H_q W^T, online LSE partials
+    // S1+S2 (+ keep q = exp(z - m_tile) of the chunk in bf16): z = H_q W^T, LSE partials
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
-      EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, Z, fp.ldv};
-      ep.use_zmap = z_tma();
-      if (ep.use_zmap) LCE_TRY(map_f32_store(&ep.zmap, Z, fp.ldv, fp.Nc, fp.ldv));
+      EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, nullptr, fp.ldv};
+      ep.store_q = 1;
+      LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
     const unsigned cb = static_cast<unsigned>(fp.Nc / kRowsPerCta);
@@ -961,14 +972,14 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
         LCE_TRY(last_error());
       }
     }
-    {  // S4 without recompute: G = s_i (softmax - onehot) from the kept logits
+    {  // S4 without recompute: G = s_i (softmax - onehot) from the kept q, in place
       LaunchScope sc(LCE_K_BWD_G, s);
-      fixup_g_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(Z, fp.ldv, Vl, r0, Nc, yc,
+      fixup_q_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(G, fp.ldv, Vl, r0, Nc, yc,
                                                                   static_cast<int32_t>(p->vocab_start), lsec,
-                                                                  row_grad ? gsc : nullptr, hdr, G);
+                                                                  row_grad ? gsc : nullptr, hdr, pm, fp.Nc, zt);
       LCE_TRY(last_error());
     }
-    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, t_h_mn, r0, Z, vdh, idx, dhidden,
+    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, t_h_mn, r0, slab, vdh, idx, dhidden,
                         dweight, q > 0 || accumulate_dweight));
   }
   {

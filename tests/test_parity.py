@@ -403,7 +403,7 @@ def test_fused_many_row_chunks_with_packed_labels(cuda_lib, variant):
     V, D = 3000, 128
     lab = packed_labels(2048, V, seed=1)[:1100]
     inp = small(1100, D, V, labels=lab)
-    budget = 256 * 6 * 3072  # Nc = 256 rows per chunk
+    budget = 256 * 2 * 3072  # Nc = 256 rows per chunk (2 bytes per chunk element)
     g = fused_run(inp, budget=budget)
     assert_parity(g, oracle_run(inp), lab)
     one = fused_run(inp)
@@ -438,7 +438,7 @@ def test_fused_single_rank_communicator_path(cuda_lib):
         lab = packed_labels(2048, 3000, seed=2)[:900]
         inp = small(900, 128, 3000, labels=lab)
         out = F.forward_backward(inp.hidden, inp.weight, inp.labels, with_token_loss=True, comm=comm,
-                                 chunk_budget_bytes=256 * 6 * 3072)
+                                 chunk_budget_bytes=256 * 2 * 3072)
         torch.cuda.synchronize()
         g = {"loss": out["loss"].item(), "n_valid": int(out["n_valid"].item()),
              "lse": out["lse"].cpu().double().numpy(), "tok": out["token_loss"].cpu().double().numpy(),
@@ -469,7 +469,7 @@ def test_vocab_shard_offsets_single_rank(cuda_lib, path):
             dh, dw = F.backward(inp.hidden, Wsh, inp.labels, out["lse"], comm=comm, vocab_start=v0, vocab_total=V)
         else:
             out = F.forward_backward(inp.hidden, Wsh, inp.labels, comm=comm, vocab_start=v0, vocab_total=V,
-                                     with_token_loss=True, chunk_budget_bytes=256 * 6 * 512)
+                                     with_token_loss=True, chunk_budget_bytes=256 * 2 * 512)
             dh, dw = out["dhidden"], out["dweight"]
         torch.cuda.synchronize()
     finally:
@@ -503,7 +503,7 @@ def test_cuda_graph_capture_replays_bitwise(cuda_lib, path):
     def step():
         if path == "fused":
             F.forward_backward(h, w, y, dhidden=dH, dweight=dW, workspace=ws, out=out,
-                               chunk_budget_bytes=256 * 6 * 5120)
+                               chunk_budget_bytes=256 * 2 * 5120)
         else:
             F.forward(h, w, y, workspace=ws, out=out)
             F.backward(h, w, y, out["lse"], dhidden=dH, dweight=dW, workspace=ws, chunk_budget_bytes=700 * 2 * 1024)
