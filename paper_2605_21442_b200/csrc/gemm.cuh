@@ -456,6 +456,210 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
+// =====================================================================
+// Wide CTA-pair variant: 512 x 256 per pair (each CTA stages 256 rows of A and
+// 128 columns of B per k-block; two cta_group::2 256x256x16 MMAs per k16 step
+// share the B operand).  25% fewer operand bytes from L2 per flop than the
+// 256 x 256 pair tile, which matters because these kernels are power-capped:
+// fewer bytes moved per MMA, higher SM clock.  The two 128-lane x 256-column
+// accumulators fill the 512 TMEM columns, so there is no second buffer; the
+// epilogue drains half 0 then half 1, and the next tile's MMAs start on half 0
+// as soon as it is drained (up to kWideStages k-blocks ahead) and catch up on
+// half 1 when that is drained.
+//   CTA r, accumulator half h holds pair-tile rows [256 r + 128 h, +128).
+// =====================================================================
+constexpr int kWideBM = 512;  // rows per wide pair tile
+constexpr int kWideStages = 4;
+constexpr int kWideAStage = 256 * BK * 2;  // 32 KB
+constexpr int kWideBStage = 128 * BK * 2;  // 16 KB
+constexpr int kWideSmemBytes = kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + kEpiSmemBytes;
+
+template <bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmDims dims, const __grid_constant__ typename Epi::Params ep) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kWideStages * kWideAStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kWideStages * kWideBStage);
+  uint64_t* empty = full + kWideStages;
+  uint64_t* tfull = empty + kWideStages;
+  uint64_t* tempty = tfull + 1;  // [2]: accumulator half drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1;
+  const int nclusters = gridDim.x >> 1;
+
+  const int M = extent(dims.m_dev, dims.m_static, dims.m_off, dims.m_cap);
+  const int K = extent(dims.k_dev, dims.k_static, dims.k_off, dims.k_cap);
+  const int N = dims.n;
+  const int num_m = (M + kWideBM - 1) / kWideBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_k = (K + BK - 1) / BK;
+  const int S = dims.ksplit > 1 ? dims.ksplit : 1;
+  const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
+  const int num_tiles = num_m * num_n * S;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kWideStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull[0], 1);
+    mbar_init(&tempty[0], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    mbar_init(&tempty[1], 8);
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, kTmemCols);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && num_k > 0) {
+      // ---------------------------------------------------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
+        const int ma = w.mb * kWideBM + 256 * rank;  // this CTA's 256 A rows
+        const int nbh = w.nb * BN + 128 * rank;      // this CTA's B rows (N half)
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kWideAStage + kWideBStage));
+          uint8_t* a = sA + stage * kWideAStage;
+          uint8_t* b = sB + stage * kWideBStage;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_2d_pair(a, &tmA, &full[stage], k0, ma, pa);
+            tma_load_2d_pair(a + 128 * 128, &tmA, &full[stage], k0, ma + 128, pa);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d_pair(a + j * BK * 128, &tmA, &full[stage], ma + 64 * j, k0, pa);
+          }
+          if (!B_MN) {
+            tma_load_2d_pair(b, &tmB, &full[stage], k0, nbh, pb);
+          } else {
+            tma_load_2d_pair(b, &tmB, &full[stage], nbh, k0, pb);
+            tma_load_2d_pair(b + BK * 128, &tmB, &full[stage], nbh + 64, k0, pb);
+          }
+          if (++stage == kWideStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------------------------------------------------- MMA issuer (leader only)
+      constexpr uint32_t idesc = idesc_bf16_f32(kPairBM, BN, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_phase = 0;
+      // MMAs of accumulator half h on the k-block in `st`
+      auto issue = [&](int st, int h, bool first) {
+        const uint32_t a_addr = smem_u32(sA + st * kWideAStage + h * (128 * 128));
+        const uint32_t b_addr = smem_u32(sB + st * kWideBStage);
+        const uint32_t d = tmem_base + h * BN;
+#pragma unroll
+        for (int kk = 0; kk < BK / UK; ++kk) {
+          const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + kk * (UK * 128), BK * 128, 1024)
+                                   : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
+          const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
+                                   : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
+          mma_bf16_ss_pair(d, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
+        }
+      };
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
+        const int nkb = w.kb1 - w.kb0;
+        const int pre = nkb < kWideStages ? nkb : kWideStages;
+        // half 0 on the first `pre` k-blocks as soon as the epilogue has drained it
+        mbar_wait_cluster(&tempty[0], acc_phase ^ 1);
+        tc_fence_after();
+        int st = stage;
+        uint32_t ph = phase;
+        for (int j = 0; j < pre; ++j) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          issue(st, 0, j == 0);
+          if (++st == kWideStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+        // half 1 catches up on the same k-blocks, then both advance together
+        mbar_wait_cluster(&tempty[1], acc_phase ^ 1);
+        tc_fence_after();
+        for (int j = 0; j < nkb; ++j) {
+          if (j >= pre) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            issue(stage, 0, false);
+          }
+          issue(stage, 1, j == 0);
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == kWideStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (nkb > 0) {
+          mma_commit_pair(&tfull[0], 0x3);
+        } else {
+          mbar_arrive_cluster(&tfull[0], 0);
+          mbar_arrive_cluster(&tfull[0], 1);
+        }
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
+      const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank);
+      TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s, epi_smem + q * kEpiWarpSmem};
+      Epi::prefetch(ep, ti);
+      ti.m0 = m0 + 128;
+      Epi::prefetch(ep, ti);
+      mbar_wait_cluster(&tfull[0], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t taddr = tmem_base + h * BN + (static_cast<uint32_t>(q * 32) << 16);
+        ti.m0 = m0 + 128 * h;
+        Epi::apply(ep, taddr, ti);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tempty[h], 0);
+      }
+      acc_phase ^= 1;
+    }
+    Epi::finish(ep);
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
+}
+
 // Loads the 32-column chunk `c` of this thread's accumulator row as floats.
 __device__ __forceinline__ void load_chunk(uint32_t taddr, int c, bool zero, float (&x)[32]) {
   uint32_t v[32];

@@ -317,11 +317,17 @@ struct EpiDW : EpiBase {
     int32_t accumulate;
     const Header* hdr;
     int32_t use_c;        // 1: scale by c; 0: c already folded into G
+    int32_t use_map;      // 1: write through `map` (fp32 32x32 boxes, 128B swizzle): TMA store,
+                          //    or TMA reduce-add when accumulating (the L2 adds; no read by the SM)
+    alignas(64) CUtensorMap map;  // [M rows of this GEMM, D] (rows / cols past it are clipped)
   };
+  static __device__ __forceinline__ void finish(const Params& p) {
+    if (p.use_map && (threadIdx.x & 31) == 0) tma_store_wait_all();
+  }
   // accumulate mode reads the old dW tile row: pull it into L2 while the MMA runs
   static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
     const int r = t.m0 + t.row;
-    if (!p.accumulate || t.zero_acc || r >= t.M) return;
+    if (p.use_map || !p.accumulate || t.zero_acc || r >= t.M) return;
     const float* row = p.dW + static_cast<int64_t>(r) * p.ld;
     for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
   }
@@ -330,6 +336,32 @@ struct EpiDW : EpiBase {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const float cs = p.use_c ? p.hdr->c : 1.f;
+    if (p.use_map) {
+      const int l = t.row & 31;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float x[32];
+        load_chunk(taddr, c, t.zero_acc, x);
+        if (t.n0 + c * 32 >= t.N) continue;  // uniform across the warp
+        if (l == 0) tma_store_wait_read();
+        __syncwarp();
+        uint8_t* st = t.smem;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
+              make_float4(cs * x[4 * v], cs * x[4 * v + 1], cs * x[4 * v + 2], cs * x[4 * v + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (l == 0) {
+          if (p.accumulate)
+            tma_reduce_add_2d(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l));
+          else
+            tma_store_2d(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l));
+          tma_store_commit();
+        }
+      }
+      return;
+    }
     float* row = p.dW + static_cast<int64_t>(r) * p.ld;
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {

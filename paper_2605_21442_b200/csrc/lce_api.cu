@@ -264,7 +264,8 @@ lce_status_t device_info(DevInfo* out) {
     // opt in to the dynamic shared memory every GEMM instantiation needs
 #define LCE_SMEM_ATTR(A, B, E)                                                                                 \
   LCE_CUDA(cudaFuncSetAttribute(gemm_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes)); \
-  LCE_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemBytes))
+  LCE_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPairSmemBytes)); \
+  LCE_CUDA(cudaFuncSetAttribute(gemm_wide_kernel<A, B, E>, cudaFuncAttributeMaxDynamicSharedMemorySize, kWideSmemBytes))
     LCE_SMEM_ATTR(false, false, EpiLse);
     LCE_SMEM_ATTR(false, false, EpiG);
     LCE_SMEM_ATTR(false, true, EpiDH);
@@ -420,6 +421,16 @@ int hint_override(int cls, char which, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
+// Wide (512 x 256) pair tiles for a GEMM class: LCE_WIDE_<class index> or
+// LCE_WIDE (1 on, 0 off) override the default.
+int use_wide(int cls, int dflt) {
+  char name[32];
+  snprintf(name, sizeof(name), "LCE_WIDE_%d", cls);
+  const char* e = getenv(name);
+  if (!e) e = getenv("LCE_WIDE");
+  return e ? atoi(e) : dflt;
+}
+
 template <bool A_MN, bool B_MN, class Epi>
 lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d_in,
                          const typename Epi::Params& ep, int sms, cudaStream_t s) {
@@ -455,7 +466,10 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
+  const bool wide = use_wide(cls, 0) != 0;
+  if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
+  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
+                       : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
   if (e != cudaSuccess) {
     if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: cudaLaunchKernelEx -> %s\n", cudaGetErrorString(e));
     return LCE_ERR_CUDA;
@@ -765,6 +779,8 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
       GemmDims d{nullptr, static_cast<int32_t>(vc), &hdr->n_valid, 0, static_cast<int32_t>(pl.D)};
       if (!adam) {
         EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
+        ep.use_map = z_tma();
+        if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight + v0 * pl.D, pl.D, vc, pl.D));
         LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
       } else {  // NEXT-2: the AdamW step of these W rows happens in the dW epilogue
         const lce_adamw_t& h = adam->hp;
@@ -821,6 +837,8 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
   {
     GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
     EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
+    ep.use_map = z_tma();
+    if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
     LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s)));
   }
   if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
