@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 from synth.inputs import CONFIGS, IGNORE, make_config  # noqa: E402
 
 METRIC = "LCE fwd+bwd tokens/sec and % bf16 tensor peak at 1/2/4/8 B200; peak HBM bytes"
+SMS = 148  # B200 SMs (dense bf16 tcgen05: 8192 flop/clk/SM)
 
 
 def peaks():
@@ -277,9 +278,20 @@ def main():
     if not fused:
         gemm_flops["bwd_g"] = 2.0 * nv * vl * D  # the recompute GEMM (fused: an HBM-bound fix-up kernel)
     dom = max(prof, key=lambda k: prof[k][0])
-    dom_ms, dom_n = prof[dom]
-    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps} for k, v in prof.items()
-               if v[1]}
+    dom_ms, dom_n = prof[dom][:2]
+    kernels = {}
+    for k, v in prof.items():
+        if not v[1]:
+            continue
+        kernels[k] = {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+        if v[2]:  # GEMM classes: SM clock inside the step (in-kernel clock64 / globaltimer probe)
+            kernels[k]["sm_mhz"] = v[2]
+            if k in gemm_flops:
+                tf = gemm_flops[k] / (v[0] / args.steps / 1e3) / 1e12
+                kernels[k]["tflops"] = tf
+                # tensor-pipe utilisation at the clock the power cap allowed: achieved / (148 SMs x
+                # 8192 dense bf16 flop/clk x that clock)
+                kernels[k]["util_at_clock"] = tf * 1e12 / (SMS * 8192 * v[2] * 1e6)
     roof = None
     if dom in gemm_flops and dom_n:
         per_launch_flops = gemm_flops[dom] * args.steps / dom_n
@@ -288,7 +300,9 @@ def main():
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             traffic = json.load(open(tp)).get(args.config + ("_fused" if fused else ""), {}).get(dom)
+        mhz = prof[dom][2]
         roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s", "frac": achieved / sus,
+                "sm_mhz": mhz, "util_at_clock": (achieved * 1e12 / (SMS * 8192 * mhz * 1e6)) if mhz else None,
                 "traffic": traffic, "kernel": dom, "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
                 "flops_per_launch": per_launch_flops,
                 "share_of_step": dom_ms / ms if world == 1 else None}

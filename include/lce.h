@@ -248,6 +248,13 @@ typedef enum {
  * it then clears the record.  Host-thread-global; not for concurrent use. */
 lce_status_t lce_profile_enable(int on);
 lce_status_t lce_profile_read(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT]);
+/* As lce_profile_read, plus for the GEMM classes the SM clock each launch ran
+ * at: CTA 0 of every profiled GEMM launch records (%globaltimer, clock64) when
+ * its mainloop starts and ends; sm_cycles / sm_ns are the summed differences
+ * per class (their ratio is the mean SM clock inside the step, which the
+ * power cap sets).  Any output pointer may be NULL.  Clears the record. */
+lce_status_t lce_profile_read_clocks(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT],
+                                     double sm_cycles[LCE_K_COUNT], double sm_ns[LCE_K_COUNT]);
 
 /* ---- diagnostics (tests only) ---------------------------------------------
  * C[M, N] (fp32, row-major, ldc = N) = A * B^T through the same tcgen05 GEMM

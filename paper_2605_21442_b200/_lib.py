@@ -26,6 +26,7 @@ EXPORTS = [
     "lce_workspace_bytes", "lce_forward", "lce_backward", "lce_check_device_status",
     "lce_comm_get_unique_id", "lce_comm_init", "lce_comm_destroy", "lce_comm_size", "lce_comm_rank",
     "lce_status_string", "lce_abi_version", "lce_launch_count", "lce_profile_enable", "lce_profile_read",
+    "lce_profile_read_clocks",
     "lce_debug_gemm", "lce_fused_workspace_bytes", "lce_forward_backward", "lce_backward_adamw",
     "lce_kd_workspace_bytes", "lce_kd_forward_backward",
 ]
@@ -104,6 +105,9 @@ def _load() -> ctypes.CDLL:
     lib.lce_profile_enable.restype = ctypes.c_int
     lib.lce_profile_read.argtypes = [P(ctypes.c_double), P(ctypes.c_int64)]
     lib.lce_profile_read.restype = ctypes.c_int
+    lib.lce_profile_read_clocks.argtypes = [P(ctypes.c_double), P(ctypes.c_int64), P(ctypes.c_double),
+                                            P(ctypes.c_double)]
+    lib.lce_profile_read_clocks.restype = ctypes.c_int
     lib.lce_debug_gemm.argtypes = [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                    ctypes.c_int, vp]
     lib.lce_debug_gemm.restype = ctypes.c_int

@@ -33,9 +33,12 @@ constexpr int kGroupM = 16;  // raster: 16 m-blocks share each n-block sweep (L2
 
 constexpr int kAStageBytes = BM * BK * 2;  // 16 KB
 constexpr int kBStageBytes = BN * BK * 2;  // 32 KB
-// Per epilogue warp: a 32 x 128-byte staging tile for TMA stores (4 warps).
+// Per epilogue warp: kEpiBufs rotating 32 x 128-byte staging tiles for TMA
+// stores (4 warps), so a tile can be refilled while the previous store still
+// reads its neighbour.
 constexpr int kEpiWarpSmem = 4096;
-constexpr int kEpiSmemBytes = 4 * kEpiWarpSmem;
+constexpr int kEpiBufs = 2;
+constexpr int kEpiSmemBytes = 4 * kEpiBufs * kEpiWarpSmem;
 // [A stages][B stages][barriers: 1 KB][epilogue staging] after 1 KB alignment
 constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 /*align slack*/ + 1024 /*barriers*/ +
                            kEpiSmemBytes;
@@ -61,7 +64,21 @@ struct GemmDims {
   // L2 eviction priority of the A / B operand loads (0 normal, 1 evict_first,
   // 2 evict_last): operands reused by later tiles of the raster stay in L2
   int32_t a_hint, b_hint;
+  // wide kernel: k-blocks accumulator half 1 trails half 0 by (0 .. kWideStages - 1)
+  int32_t wide_lag;
+  // profiler (null = off): CTA 0 records {globaltimer, clock64} at start and
+  // end, i.e. the SM clock the kernel actually ran at inside the step
+  unsigned long long* probe;
 };
+
+__device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
+  if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    probe[at] = t;
+    probe[at + 1] = clock64();
+  }
+}
 
 // Geometry handed to the epilogue for one output tile.
 struct TileInfo {
@@ -70,8 +87,21 @@ struct TileInfo {
   int row;        // row of this thread inside the tile (== TMEM lane)
   bool zero_acc;  // empty k-range: the accumulator was never written, treat as 0
   int split;      // split-K index of this work item
-  uint8_t* smem;  // this warp's 4 KB epilogue staging tile (1 KB aligned)
+  uint8_t* smem;  // this warp's kEpiBufs x 4 KB epilogue staging tiles (1 KB aligned)
+  uint32_t nst;   // TMA stores this warp has issued so far (selects the next staging tile)
 };
+
+// This warp's next staging tile: waits (lane 0) until the store that last read
+// it is done reading, i.e. at most kEpiBufs - 1 newer stores may still be
+// reading.  Every call must be followed by exactly one committed store group.
+__device__ __forceinline__ uint8_t* stage_next(TileInfo& t) {
+  static_assert(kEpiBufs == 2, "wait depth below assumes two staging tiles");
+  if ((t.row & 31) == 0) tma_store_wait_read_1();
+  __syncwarp();
+  uint8_t* st = t.smem + (t.nst & (kEpiBufs - 1)) * kEpiWarpSmem;
+  ++t.nst;
+  return st;
+}
 
 // Epilogue policies derive from EpiBase; `prefetch` runs before the epilogue
 // waits for the tile's accumulator (i.e. while the MMA is still computing it),
@@ -171,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  probe_mark(dims.probe, 0);
 
   if (warp == 0) {
     if (lane == 0 && num_k > 0) {
@@ -254,15 +285,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t nst = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kEpiWarpSmem};
+                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
       Epi::prefetch(ep, ti);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       Epi::apply(ep, taddr, ti);
+      nst = ti.nst;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -275,6 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  probe_mark(dims.probe, 2);
   if (warp == 2) tmem_dealloc(tmem_base, kTmemCols);
 }
 
@@ -349,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  probe_mark(dims.probe, 0);
 
   if (warp == 0) {
     if (lane == 0 && num_k > 0) {
@@ -432,15 +467,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t nst = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
-                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiWarpSmem};
+                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
       Epi::prefetch(ep, ti);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       Epi::apply(ep, taddr, ti);
+      nst = ti.nst;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
@@ -453,23 +490,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  probe_mark(dims.probe, 2);
   if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 
 // =====================================================================
 // Wide CTA-pair variant: 512 x 256 per pair (each CTA stages 256 rows of A and
-// 128 columns of B per k-block; two cta_group::2 256x256x16 MMAs per k16 step
-// share the B operand).  25% fewer operand bytes from L2 per flop than the
-// 256 x 256 pair tile, which matters because these kernels are power-capped:
-// fewer bytes moved per MMA, higher SM clock.  The two 128-lane x 256-column
-// accumulators fill the 512 TMEM columns, so there is no second buffer; the
-// epilogue drains half 0 then half 1, and the next tile's MMAs start on half 0
-// as soon as it is drained (up to kWideStages k-blocks ahead) and catch up on
-// half 1 when that is drained.
+// 128 columns of B per k-block; two cta_group::2 256x256x16 MMAs per k16 step,
+// one per accumulator half, share the B operand).  25% fewer operand bytes
+// from L2 per flop than the 256 x 256 pair tile, which matters because these
+// kernels are power-capped: fewer bytes moved per MMA, higher SM clock.
 //   CTA r, accumulator half h holds pair-tile rows [256 r + 128 h, +128).
+// The two 128-lane x 256-column halves fill the 512 TMEM columns, so there is
+// no second buffer.  Instead the halves are drained and refilled out of step:
+// the MMA thread keeps two cursors over the same k-block sequence, half 1
+// trailing half 0 by up to wide_lag k-blocks (the ring keeps a stage until
+// half 1 has read it).  When half 0 finishes a tile, the epilogue drains it
+// while half 1 completes its trailing k-blocks; half 0 then starts the next
+// tile while half 1 is drained, and so on -- each half's epilogue overlaps the
+// other half's MMAs instead of stalling the tensor pipe.
 // =====================================================================
 constexpr int kWideBM = 512;  // rows per wide pair tile
 constexpr int kWideStages = 4;
+constexpr int kWideLag = 2;   // default k-blocks half 1 trails half 0 by (GemmDims::wide_lag)
 constexpr int kWideAStage = 256 * BK * 2;  // 32 KB
 constexpr int kWideBStage = 128 * BK * 2;  // 16 KB
 constexpr int kWideSmemBytes = kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + kEpiSmemBytes;
@@ -484,8 +527,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + kWideStages * kWideAStage;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + kWideStages * kWideBStage);
   uint64_t* empty = full + kWideStages;
-  uint64_t* tfull = empty + kWideStages;
-  uint64_t* tempty = tfull + 1;  // [2]: accumulator half drained
+  uint64_t* tfull = empty + kWideStages;  // [2]: accumulator half computed
+  uint64_t* tempty = tfull + 2;           // [2]: accumulator half drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
@@ -513,9 +556,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&tfull[0], 1);
-    mbar_init(&tempty[0], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
-    mbar_init(&tempty[1], 8);
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&tfull[h], 1);   // multicast commit
+      mbar_init(&tempty[h], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -526,6 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  probe_mark(dims.probe, 0);
 
   if (warp == 0) {
     if (lane == 0 && num_k > 0) {
@@ -567,10 +612,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer (leader only)
       constexpr uint32_t idesc = idesc_bf16_f32(kPairBM, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t acc_phase = 0;
-      // MMAs of accumulator half h on the k-block in `st`
+      // MMAs of accumulator half h on the k-block in stage `st`
       auto issue = [&](int st, int h, bool first) {
         const uint32_t a_addr = smem_u32(sA + st * kWideAStage + h * (128 * 128));
         const uint32_t b_addr = smem_u32(sB + st * kWideBStage);
@@ -584,64 +626,114 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16_ss_pair(d, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
         }
       };
-      for (int t = cluster; t < num_tiles; t += nclusters) {
+      auto nkb_of = [&](int t) {
+        if (t >= num_tiles) return 0;
         const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-        const int nkb = w.kb1 - w.kb0;
-        const int pre = nkb < kWideStages ? nkb : kWideStages;
-        // half 0 on the first `pre` k-blocks as soon as the epilogue has drained it
-        mbar_wait_cluster(&tempty[0], acc_phase ^ 1);
-        tc_fence_after();
-        int st = stage;
-        uint32_t ph = phase;
-        for (int j = 0; j < pre; ++j) {
-          mbar_wait(&full[st], ph);
-          tc_fence_after();
-          issue(st, 0, j == 0);
-          if (++st == kWideStages) {
-            st = 0;
-            ph ^= 1;
+        return w.kb1 - w.kb0;
+      };
+      // per half: work item, k-block within it, its k-block count, parity of
+      // the drain to wait for, whether that drain has been seen
+      int th[2] = {cluster, cluster}, jh[2] = {0, 0};
+      int nk[2];
+      nk[0] = nk[1] = nkb_of(cluster);
+      uint32_t tph[2] = {0, 0};
+      bool tok[2] = {false, false};
+      int st0 = 0, st1 = 0;  // ring stage of each half's next k-block
+      uint32_t ph0 = 0;      // full-barrier parity of half 0's next stage
+      long long g0 = 0, g1 = 0;  // k-blocks issued per half (same global sequence)
+      const int lag = dims.wide_lag < 0 ? 0 : (dims.wide_lag >= kWideStages ? kWideStages - 1 : dims.wide_lag);
+      auto next_tile = [&](int h) {
+        th[h] += nclusters;
+        jh[h] = 0;
+        tph[h] ^= 1;
+        tok[h] = false;
+        nk[h] = nkb_of(th[h]);
+      };
+      while (th[0] < num_tiles || th[1] < num_tiles) {
+        bool progress = false;
+        // ---- half 0 leads: needs its accumulator drained and the stage loaded
+        if (th[0] < num_tiles) {
+          if (jh[0] == 0 && !tok[0]) tok[0] = mbar_test_cluster(&tempty[0], tph[0] ^ 1);
+          if (tok[0]) {
+            if (nk[0] == 0) {  // empty k-range: the epilogue treats the half as zero
+              mbar_arrive_cluster(&tfull[0], 0);
+              mbar_arrive_cluster(&tfull[0], 1);
+              next_tile(0);
+              progress = true;
+            } else if (mbar_test(&full[st0], ph0)) {
+              tc_fence_after();
+              issue(st0, 0, jh[0] == 0);
+              if (++st0 == kWideStages) {
+                st0 = 0;
+                ph0 ^= 1;
+              }
+              ++g0;
+              progress = true;
+              if (++jh[0] == nk[0]) {
+                mma_commit_pair(&tfull[0], 0x3);
+                next_tile(0);
+              }
+            }
           }
         }
-        // half 1 catches up on the same k-blocks, then both advance together
-        mbar_wait_cluster(&tempty[1], acc_phase ^ 1);
-        tc_fence_after();
-        for (int j = 0; j < nkb; ++j) {
-          if (j >= pre) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            issue(stage, 0, false);
-          }
-          issue(stage, 1, j == 0);
-          mma_commit_pair(&empty[stage], 0x3);
-          if (++stage == kWideStages) {
-            stage = 0;
-            phase ^= 1;
+        // ---- half 1 trails: stages half 0 has already read.  It stays
+        // `lag` k-blocks behind, and catches up only while half 0 waits for
+        // its own drain (or is done): those trailing k-blocks are what the
+        // tensor pipe runs while the epilogue drains half 0.  (Half 0 never
+        // waits on a stage half 1 has not yet read: lag < kWideStages.)
+        const bool h0_draining = th[0] >= num_tiles || (jh[0] == 0 && !tok[0]);
+        if (th[1] < num_tiles && (h0_draining || g0 - g1 > lag)) {
+          if (jh[1] == 0 && !tok[1]) tok[1] = mbar_test_cluster(&tempty[1], tph[1] ^ 1);
+          if (tok[1]) {
+            if (nk[1] == 0) {
+              mbar_arrive_cluster(&tfull[1], 0);
+              mbar_arrive_cluster(&tfull[1], 1);
+              next_tile(1);
+              progress = true;
+            } else if (g1 < g0) {
+              tc_fence_after();
+              issue(st1, 1, jh[1] == 0);
+              mma_commit_pair(&empty[st1], 0x3);  // both halves have read this stage
+              if (++st1 == kWideStages) st1 = 0;
+              ++g1;
+              progress = true;
+              if (++jh[1] == nk[1]) {
+                mma_commit_pair(&tfull[1], 0x3);
+                next_tile(1);
+              }
+            }
           }
         }
-        if (nkb > 0) {
-          mma_commit_pair(&tfull[0], 0x3);
-        } else {
-          mbar_arrive_cluster(&tfull[0], 0);
-          mbar_arrive_cluster(&tfull[0], 1);
+        // Nothing issuable: suspend (try_wait, not a test_wait spin that would
+        // compete with the TMA / MMA traffic on the barriers) on what the
+        // leading half waits for; then re-evaluate both halves.
+        if (!progress) {
+          if (th[0] < num_tiles && tok[0])
+            mbar_try_wait(smem_u32(&full[st0]), ph0);
+          else if (th[0] < num_tiles)
+            mbar_try_wait_cluster(&tempty[0], tph[0] ^ 1);
+          else
+            mbar_try_wait_cluster(&tempty[1], tph[1] ^ 1);
         }
-        acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;
     uint32_t acc_phase = 0;
+    uint32_t nst = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank);
-      TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s, epi_smem + q * kEpiWarpSmem};
+      TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
+                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
       Epi::prefetch(ep, ti);
       ti.m0 = m0 + 128;
       Epi::prefetch(ep, ti);
-      mbar_wait_cluster(&tfull[0], acc_phase);
-      tc_fence_after();
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
+        mbar_wait_cluster(&tfull[h], acc_phase);
+        tc_fence_after();
         const uint32_t taddr = tmem_base + h * BN + (static_cast<uint32_t>(q * 32) << 16);
         ti.m0 = m0 + 128 * h;
         Epi::apply(ep, taddr, ti);
@@ -649,6 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tempty[h], 0);
       }
+      nst = ti.nst;
       acc_phase ^= 1;
     }
     Epi::finish(ep);
@@ -657,6 +750,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  probe_mark(dims.probe, 2);
   if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
 }
 

@@ -60,11 +60,9 @@ struct EpiLse : EpiBase {
   // unit v of row l at unit v ^ (l & 7)) and let lane 0 issue the TMA store
   // at (col, row0).  Rows >= M are stored too (never read); rows past the
   // buffer are clipped.
-  static __device__ __forceinline__ void tma_rows(const Params& p, const TileInfo& t, int col, const uint4 (&u)[8]) {
+  static __device__ __forceinline__ void tma_rows(const Params& p, TileInfo& t, int col, const uint4 (&u)[8]) {
     const int l = t.row & 31;
-    if (l == 0) tma_store_wait_read();  // the previous store has consumed the staging tile
-    __syncwarp();
-    uint8_t* st = t.smem;
+    uint8_t* st = stage_next(t);  // a staging tile no pending store still reads
 #pragma unroll
     for (int v = 0; v < 8; ++v) *reinterpret_cast<uint4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) = u[v];
     fence_async_smem();
@@ -75,7 +73,7 @@ struct EpiLse : EpiBase {
     }
   }
   template <bool kStoreQ>
-  static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, const TileInfo& t, float ml) {
+  static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, TileInfo& t, float ml) {
     float s = 0.f;
 #pragma unroll 1
     for (int c2 = 0; c2 < BN / 64; ++c2) {
@@ -105,7 +103,7 @@ struct EpiLse : EpiBase {
     }
     return s;
   }
-  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[p.row_off + r] - p.label_off - t.n0) : -1;  // tile-relative target column
@@ -186,7 +184,7 @@ struct EpiG : EpiBase {
       w[j / 2] = pack_bf16x2(g0, g1);
     }
   }
-  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[r] - p.label_off - t.n0) : -1;
@@ -203,9 +201,7 @@ struct EpiG : EpiBase {
         uint32_t w[32];
         g_chunk(p, taddr, t, 2 * c2, valid, yl, lsel, rs, w);
         g_chunk(p, taddr, t, 2 * c2 + 1, valid, yl, lsel, rs, w + 16);
-        if (l == 0) tma_store_wait_read();
-        __syncwarp();
-        uint8_t* st = t.smem;
+        uint8_t* st = stage_next(t);
 #pragma unroll
         for (int v = 0; v < 8; ++v)
           *reinterpret_cast<uint4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
@@ -331,7 +327,7 @@ struct EpiDW : EpiBase {
     const float* row = p.dW + static_cast<int64_t>(r) * p.ld;
     for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
   }
-  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     if (t.zero_acc && p.accumulate) return;  // K == 0 adds nothing (uniform across the CTA)
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
@@ -343,9 +339,7 @@ struct EpiDW : EpiBase {
         float x[32];
         load_chunk(taddr, c, t.zero_acc, x);
         if (t.n0 + c * 32 >= t.N) continue;  // uniform across the warp
-        if (l == 0) tma_store_wait_read();
-        __syncwarp();
-        uint8_t* st = t.smem;
+        uint8_t* st = stage_next(t);
 #pragma unroll
         for (int v = 0; v < 8; ++v)
           *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =

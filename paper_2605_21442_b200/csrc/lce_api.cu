@@ -118,13 +118,14 @@ struct FusedPlan {
 };
 
 int use_pair_units(int sms);
+int tile_rows(int cls);
 
 // Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
 // work items fill the persistent grid's last wave to >= 97% (else the best).
 // `max_split` bounds it where the fp32 slabs alias another buffer.
 int dh_split(int64_t Nc, int64_t D, int max_split, int sms) {
   const int64_t units = use_pair_units(sms);
-  const int64_t rows = units == sms ? 128 : 256;
+  const int64_t rows = tile_rows(LCE_K_BWD_DH);
   const int64_t tiles = ceil_div(Nc, rows) * ceil_div(D, BN);
   int best = 1;
   double best_eff = 0.0;
@@ -335,12 +336,29 @@ lce_status_t map_mnmajor(CUtensorMap* m, const void* base, int64_t K, int64_t MN
 struct ProfRec {
   int cls;
   cudaEvent_t a, b;
+  int slot;  // clock-probe slot of a GEMM launch, -1 otherwise
 };
+// clock probes of profiled GEMM launches: {t0 ns, clock0, t1 ns, clock1}
+constexpr int kProbeSlots = 4096;
+__device__ unsigned long long g_probe[kProbeSlots][4];
 struct Profiler {
   std::mutex mu;
   bool on = false;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
+  int next_slot = 0;
+  unsigned long long* probe_base = nullptr;
+  // next probe slot (wraps; profile_read is expected well before 4096 GEMMs)
+  unsigned long long* take_slot(int* slot) {
+    if (!probe_base && cudaGetSymbolAddress(reinterpret_cast<void**>(&probe_base), g_probe) != cudaSuccess) {
+      probe_base = nullptr;
+      *slot = -1;
+      return nullptr;
+    }
+    *slot = next_slot;
+    next_slot = (next_slot + 1) % kProbeSlots;
+    return probe_base + 4 * *slot;
+  }
   cudaEvent_t get() {
     if (!pool.empty()) {
       cudaEvent_t e = pool.back();
@@ -357,6 +375,7 @@ struct LaunchScope {
   int cls;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
+  int slot = -1;
   LaunchScope(int c, cudaStream_t st) : cls(c), s(st) {
     if (g_prof.on) {
       a = g_prof.get();
@@ -364,11 +383,13 @@ struct LaunchScope {
       cudaEventRecord(a, s);
     }
   }
+  // GEMM launches: the clock-probe record for this launch (null when not profiling)
+  unsigned long long* probe() { return a ? g_prof.take_slot(&slot) : nullptr; }
   ~LaunchScope() {
     g_launches.fetch_add(cls == LCE_K_COMM ? 0 : 1);
     if (a) {
       cudaEventRecord(b, s);
-      g_prof.recs.push_back({cls, a, b});
+      g_prof.recs.push_back({cls, a, b, slot});
     }
   }
 };
@@ -421,14 +442,38 @@ int hint_override(int cls, char which, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-// Wide (512 x 256) pair tiles for a GEMM class: LCE_WIDE_<class index> or
-// LCE_WIDE (1 on, 0 off) override the default.
+// Wide (512 x 256) pair tiles per GEMM class by default: the dH / dW GEMMs,
+// whose epilogues are short enough to hide behind the other accumulator half
+// (measured: DESIGN.md section 5).  LCE_WIDE_<class index> or LCE_WIDE (1 on,
+// 0 off) override; LCE_GEMM=pair / wide force one tile shape for every class.
+constexpr int kWideDefault[LCE_K_COUNT] = {0, 0, 0, 0, 0, 1, 1, 0, 0};
 int use_wide(int cls, int dflt) {
   char name[32];
   snprintf(name, sizeof(name), "LCE_WIDE_%d", cls);
   const char* e = getenv(name);
   if (!e) e = getenv("LCE_WIDE");
-  return e ? atoi(e) : dflt;
+  if (e) return atoi(e);
+  const char* g = getenv("LCE_GEMM");
+  if (g && strcmp(g, "pair") == 0) return 0;
+  if (g && strcmp(g, "wide") == 0) return 1;
+  return dflt;
+}
+// Wide kernel: k-blocks accumulator half 1 trails half 0 (gemm.cuh).  A lag
+// lets one half's epilogue overlap the other half's MMAs but takes ring stages
+// away from the TMA prefetch: 0 for dH (K = V_l, the epilogue is negligible).
+// LCE_WIDE_LAG_<class index> / LCE_WIDE_LAG override.
+constexpr int kWideLagDefault[LCE_K_COUNT] = {1, 1, 1, 1, 1, 0, 1, 1, 1};
+int wide_lag(int cls) {
+  char name[32];
+  snprintf(name, sizeof(name), "LCE_WIDE_LAG_%d", cls);
+  const char* e = getenv(name);
+  if (!e) e = getenv("LCE_WIDE_LAG");
+  return e ? atoi(e) : kWideLagDefault[cls];
+}
+// rows of one output tile (one persistent work unit) of a GEMM class
+int tile_rows(int cls) {
+  if (!use_pair()) return BM;
+  return use_wide(cls, kWideDefault[cls]) ? kWideBM : kPairBM;
 }
 
 template <bool A_MN, bool B_MN, class Epi>
@@ -450,6 +495,7 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   d.a_hint = hint_override(cls, 'A', 0);
   d.b_hint = hint_override(cls, 'B', 0);
   LaunchScope sc(cls, s);
+  d.probe = sc.probe();
   if (!use_pair()) {
     gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
     return last_error();
@@ -466,7 +512,8 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const bool wide = use_wide(cls, 0) != 0;
+  const bool wide = use_wide(cls, kWideDefault[cls]) != 0;
+  d.wide_lag = wide_lag(cls);
   if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
   cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
                        : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
@@ -1228,24 +1275,44 @@ lce_status_t lce_profile_enable(int on) {
   return LCE_OK;
 }
 
-lce_status_t lce_profile_read(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT]) {
+lce_status_t lce_profile_read_clocks(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT],
+                                     double sm_cycles[LCE_K_COUNT], double sm_ns[LCE_K_COUNT]) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   for (int i = 0; i < LCE_K_COUNT; ++i) {
     if (ms) ms[i] = 0.0;
     if (launches) launches[i] = 0;
+    if (sm_cycles) sm_cycles[i] = 0.0;
+    if (sm_ns) sm_ns[i] = 0.0;
   }
   lce_status_t st = LCE_OK;
+  static unsigned long long host_probe[kProbeSlots][4];
+  bool have_probe = false;
   for (ProfRec& r : g_prof.recs) {
     float t = 0.f;
     if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
       st = LCE_ERR_CUDA;
     if (ms) ms[r.cls] += t;
     if (launches) launches[r.cls] += 1;
+    if (r.slot >= 0 && (sm_cycles || sm_ns)) {
+      if (!have_probe) {
+        if (cudaMemcpyFromSymbol(host_probe, g_probe, sizeof(host_probe)) != cudaSuccess) st = LCE_ERR_CUDA;
+        have_probe = true;
+      }
+      const unsigned long long* q = host_probe[r.slot];
+      if (q[2] > q[0] && q[3] > q[1]) {
+        if (sm_ns) sm_ns[r.cls] += static_cast<double>(q[2] - q[0]);
+        if (sm_cycles) sm_cycles[r.cls] += static_cast<double>(q[3] - q[1]);
+      }
+    }
     g_prof.pool.push_back(r.a);
     g_prof.pool.push_back(r.b);
   }
   g_prof.recs.clear();
   return st;
+}
+
+lce_status_t lce_profile_read(double ms[LCE_K_COUNT], int64_t launches[LCE_K_COUNT]) {
+  return lce_profile_read_clocks(ms, launches, nullptr, nullptr);
 }
 
 lce_status_t lce_debug_gemm(const uint16_t* A, const uint16_t* B, float* C, int64_t M, int64_t N, int64_t K,

@@ -375,7 +375,11 @@ def profile_enable(on: bool = True) -> None:
 
 
 def profile_read() -> dict:
+    """{class: (device ms, launches, mean SM MHz of its GEMM launches or None)}
+    since profile_enable(); clears the record."""
     ms = (ctypes.c_double * LCE_K_COUNT)()
     n = (ctypes.c_int64 * LCE_K_COUNT)()
-    check(lib.lce_profile_read(ms, n), "lce_profile_read")
-    return {k: (ms[i], n[i]) for i, k in enumerate(KERNEL_CLASSES)}
+    cyc = (ctypes.c_double * LCE_K_COUNT)()
+    ns = (ctypes.c_double * LCE_K_COUNT)()
+    check(lib.lce_profile_read_clocks(ms, n, cyc, ns), "lce_profile_read_clocks")
+    return {k: (ms[i], n[i], (cyc[i] / ns[i] * 1e3) if ns[i] > 0 else None) for i, k in enumerate(KERNEL_CLASSES)}

@@ -44,7 +44,7 @@ def breakdown(fn):
     fn()
     torch.cuda.synchronize()
     F.profile_enable(False)
-    return {k: round(ms, 3) for k, (ms, n) in F.profile_read().items() if n}
+    return {k: round(v[0], 3) for k, v in F.profile_read().items() if v[1]}
 
 
 def main():
