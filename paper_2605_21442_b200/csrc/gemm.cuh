@@ -64,8 +64,6 @@ struct GemmDims {
   // L2 eviction priority of the A / B operand loads (0 normal, 1 evict_first,
   // 2 evict_last): operands reused by later tiles of the raster stay in L2
   int32_t a_hint, b_hint;
-  // wide kernel: k-blocks accumulator half 1 trails half 0 by (0 .. kWideStages - 1)
-  int32_t wide_lag;
   // profiler (null = off): CTA 0 records {globaltimer, clock64} at start and
   // end, i.e. the SM clock the kernel actually ran at inside the step
   unsigned long long* probe;
@@ -502,17 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 // kernels are power-capped: fewer bytes moved per MMA, higher SM clock.
 //   CTA r, accumulator half h holds pair-tile rows [256 r + 128 h, +128).
 // The two 128-lane x 256-column halves fill the 512 TMEM columns, so there is
-// no second buffer.  Instead the halves are drained and refilled out of step:
-// the MMA thread keeps two cursors over the same k-block sequence, half 1
-// trailing half 0 by up to wide_lag k-blocks (the ring keeps a stage until
-// half 1 has read it).  When half 0 finishes a tile, the epilogue drains it
-// while half 1 completes its trailing k-blocks; half 0 then starts the next
-// tile while half 1 is drained, and so on -- each half's epilogue overlaps the
-// other half's MMAs instead of stalling the tensor pipe.
+// no second buffer: half 0 gets its own full / empty barriers so the epilogue
+// drains it while the MMA finishes half 1's last k-block, and the next tile's
+// MMAs start on half 0 as soon as it is drained (up to kWideStages k-blocks
+// ahead) and catch up on half 1 when that is drained.  (A design in which half
+// 1 trails half 0 by a few k-blocks throughout, to overlap each half's drain
+// with the other's MMAs, ran at 65-83% tensor utilisation: the trailing
+// k-blocks hold ring stages the TMA needs for prefetch.)
 // =====================================================================
 constexpr int kWideBM = 512;  // rows per wide pair tile
 constexpr int kWideStages = 4;
-constexpr int kWideLag = 2;   // default k-blocks half 1 trails half 0 by (GemmDims::wide_lag)
 constexpr int kWideAStage = 256 * BK * 2;  // 32 KB
 constexpr int kWideBStage = 128 * BK * 2;  // 16 KB
 constexpr int kWideSmemBytes = kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + kEpiSmemBytes;
@@ -626,95 +623,56 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16_ss_pair(d, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
         }
       };
-      auto nkb_of = [&](int t) {
-        if (t >= num_tiles) return 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
         const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-        return w.kb1 - w.kb0;
-      };
-      // per half: work item, k-block within it, its k-block count, parity of
-      // the drain to wait for, whether that drain has been seen
-      int th[2] = {cluster, cluster}, jh[2] = {0, 0};
-      int nk[2];
-      nk[0] = nk[1] = nkb_of(cluster);
-      uint32_t tph[2] = {0, 0};
-      bool tok[2] = {false, false};
-      int st0 = 0, st1 = 0;  // ring stage of each half's next k-block
-      uint32_t ph0 = 0;      // full-barrier parity of half 0's next stage
-      long long g0 = 0, g1 = 0;  // k-blocks issued per half (same global sequence)
-      const int lag = dims.wide_lag < 0 ? 0 : (dims.wide_lag >= kWideStages ? kWideStages - 1 : dims.wide_lag);
-      auto next_tile = [&](int h) {
-        th[h] += nclusters;
-        jh[h] = 0;
-        tph[h] ^= 1;
-        tok[h] = false;
-        nk[h] = nkb_of(th[h]);
-      };
-      while (th[0] < num_tiles || th[1] < num_tiles) {
-        bool progress = false;
-        // ---- half 0 leads: needs its accumulator drained and the stage loaded
-        if (th[0] < num_tiles) {
-          if (jh[0] == 0 && !tok[0]) tok[0] = mbar_test_cluster(&tempty[0], tph[0] ^ 1);
-          if (tok[0]) {
-            if (nk[0] == 0) {  // empty k-range: the epilogue treats the half as zero
-              mbar_arrive_cluster(&tfull[0], 0);
-              mbar_arrive_cluster(&tfull[0], 1);
-              next_tile(0);
-              progress = true;
-            } else if (mbar_test(&full[st0], ph0)) {
-              tc_fence_after();
-              issue(st0, 0, jh[0] == 0);
-              if (++st0 == kWideStages) {
-                st0 = 0;
-                ph0 ^= 1;
-              }
-              ++g0;
-              progress = true;
-              if (++jh[0] == nk[0]) {
-                mma_commit_pair(&tfull[0], 0x3);
-                next_tile(0);
-              }
-            }
+        const int nkb = w.kb1 - w.kb0;
+        const int pre = nkb < kWideStages ? nkb : kWideStages;
+        // half 0 on the first `pre` k-blocks as soon as the epilogue has drained it
+        mbar_wait_cluster(&tempty[0], acc_phase ^ 1);
+        tc_fence_after();
+        int st = stage;
+        uint32_t ph = phase;
+        for (int j = 0; j < pre; ++j) {
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          issue(st, 0, j == 0);
+          if (++st == kWideStages) {
+            st = 0;
+            ph ^= 1;
           }
         }
-        // ---- half 1 trails: stages half 0 has already read.  It stays
-        // `lag` k-blocks behind, and catches up only while half 0 waits for
-        // its own drain (or is done): those trailing k-blocks are what the
-        // tensor pipe runs while the epilogue drains half 0.  (Half 0 never
-        // waits on a stage half 1 has not yet read: lag < kWideStages.)
-        const bool h0_draining = th[0] >= num_tiles || (jh[0] == 0 && !tok[0]);
-        if (th[1] < num_tiles && (h0_draining || g0 - g1 > lag)) {
-          if (jh[1] == 0 && !tok[1]) tok[1] = mbar_test_cluster(&tempty[1], tph[1] ^ 1);
-          if (tok[1]) {
-            if (nk[1] == 0) {
-              mbar_arrive_cluster(&tfull[1], 0);
-              mbar_arrive_cluster(&tfull[1], 1);
-              next_tile(1);
-              progress = true;
-            } else if (g1 < g0) {
-              tc_fence_after();
-              issue(st1, 1, jh[1] == 0);
-              mma_commit_pair(&empty[st1], 0x3);  // both halves have read this stage
-              if (++st1 == kWideStages) st1 = 0;
-              ++g1;
-              progress = true;
-              if (++jh[1] == nk[1]) {
-                mma_commit_pair(&tfull[1], 0x3);
-                next_tile(1);
-              }
-            }
+        if (pre == nkb && nkb > 0) mma_commit_pair(&tfull[0], 0x3);
+        // half 1 catches up on the same k-blocks (while half 1 is drained, the
+        // tensor pipe has half 0's `pre` k-blocks), then both advance together
+        mbar_wait_cluster(&tempty[1], acc_phase ^ 1);
+        tc_fence_after();
+        for (int j = 0; j < nkb; ++j) {
+          if (j >= pre) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            issue(stage, 0, false);
+            // half 0 is complete: its epilogue may start while half 1 finishes
+            if (j == nkb - 1) mma_commit_pair(&tfull[0], 0x3);
+          }
+          issue(stage, 1, j == 0);
+          mma_commit_pair(&empty[stage], 0x3);
+          if (++stage == kWideStages) {
+            stage = 0;
+            phase ^= 1;
           }
         }
-        // Nothing issuable: suspend (try_wait, not a test_wait spin that would
-        // compete with the TMA / MMA traffic on the barriers) on what the
-        // leading half waits for; then re-evaluate both halves.
-        if (!progress) {
-          if (th[0] < num_tiles && tok[0])
-            mbar_try_wait(smem_u32(&full[st0]), ph0);
-          else if (th[0] < num_tiles)
-            mbar_try_wait_cluster(&tempty[0], tph[0] ^ 1);
-          else
-            mbar_try_wait_cluster(&tempty[1], tph[1] ^ 1);
+        if (nkb > 0) {
+          mma_commit_pair(&tfull[1], 0x3);
+        } else {  // empty k-range: the epilogue treats both halves as zero
+          for (int h = 0; h < 2; ++h) {
+            mbar_arrive_cluster(&tfull[h], 0);
+            mbar_arrive_cluster(&tfull[h], 1);
+          }
         }
+        acc_phase ^= 1;
       }
     }
   } else if (warp >= 4) {

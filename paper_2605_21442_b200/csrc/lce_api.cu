@@ -108,24 +108,34 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
 constexpr int64_t kDefaultFusedBudget = 2ll << 30;
 constexpr int64_t kDefaultKdBudget = 4ll << 30;
 constexpr int kPlanSms = 148;  // B200: the split-K choice is made at plan time (host-pure sizes)
+// dH / dW GEMMs use 512 x 256 wide pair tiles when the token rows they reduce
+// over (the fused row chunk, or all tokens in the recompute path) number at
+// least this many: shorter k-ranges leave the epilogue of the wide kernel's
+// single accumulator exposed (measured: DESIGN.md section 5)
+constexpr int64_t kWideMinRows = 8192;
 
 struct FusedPlan {
   int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
   int split;                       // split-K factor of the chunk's dH GEMM
+  int wide_dh, wide_dw;            // 512 x 256 tiles for the chunk's dH / dW GEMMs
   size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, slab;
   size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
   size_t total;
 };
 
 int use_pair_units(int sms);
-int tile_rows(int cls);
+int use_wide(int cls, int dflt);
+bool use_pair();
 
 // Split-K factor of the fused path's dH GEMM: the smallest split in 1..8 whose
 // work items fill the persistent grid's last wave to >= 97% (else the best).
 // `max_split` bounds it where the fp32 slabs alias another buffer.
-int dh_split(int64_t Nc, int64_t D, int max_split, int sms) {
+int dh_split(int64_t Nc, int64_t D, int max_split, int sms, int64_t rows) {
+  if (const char* e = getenv("LCE_DH_SPLIT")) {  // tuning override
+    const int v = atoi(e);
+    return v < 1 ? 1 : (v > max_split ? max_split : v);
+  }
   const int64_t units = use_pair_units(sms);
-  const int64_t rows = tile_rows(LCE_K_BWD_DH);
   const int64_t tiles = ceil_div(Nc, rows) * ceil_div(D, BN);
   int best = 1;
   double best_eff = 0.0;
@@ -160,7 +170,12 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   if (nc_max > q.cap) nc_max = q.cap;
   q.n_chunks = ceil_div(q.cap, nc_max);
   q.Nc = round_up(ceil_div(q.cap, q.n_chunks), kPairBM);  // balanced chunks
-  q.split = dh_split(q.Nc, q.D, kd ? static_cast<int>(q.ldv / q.D) : 8, kPlanSms);
+  // wide tiles pay off once a dW work item's K (= the chunk's rows) is long
+  // enough to hide the epilogue of the unbuffered accumulator
+  q.wide_dh = use_pair() && use_wide(LCE_K_BWD_DH, q.Nc >= kWideMinRows ? 1 : 0);
+  q.wide_dw = use_pair() && use_wide(LCE_K_BWD_DW, q.Nc >= kWideMinRows ? 1 : 0);
+  q.split = dh_split(q.Nc, q.D, kd ? static_cast<int>(q.ldv / q.D) : 8, kPlanSms,
+                     !use_pair() ? BM : (q.wide_dh ? kWideBM : kPairBM));
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -442,11 +457,10 @@ int hint_override(int cls, char which, int dflt) {
   return e ? atoi(e) : dflt;
 }
 
-// Wide (512 x 256) pair tiles per GEMM class by default: the dH / dW GEMMs,
-// whose epilogues are short enough to hide behind the other accumulator half
-// (measured: DESIGN.md section 5).  LCE_WIDE_<class index> or LCE_WIDE (1 on,
-// 0 off) override; LCE_GEMM=pair / wide force one tile shape for every class.
-constexpr int kWideDefault[LCE_K_COUNT] = {0, 0, 0, 0, 0, 1, 1, 0, 0};
+// Wide (512 x 256) pair tiles: chosen per call site (launch_gemm's wide_pref:
+// the fused path's dH / dW and the recompute path's dW when there are enough
+// token rows, kWideMinRows).  LCE_WIDE_<class index> or LCE_WIDE (1 on, 0 off)
+// override; LCE_GEMM=pair / wide force one tile shape for every GEMM.
 int use_wide(int cls, int dflt) {
   char name[32];
   snprintf(name, sizeof(name), "LCE_WIDE_%d", cls);
@@ -458,27 +472,12 @@ int use_wide(int cls, int dflt) {
   if (g && strcmp(g, "wide") == 0) return 1;
   return dflt;
 }
-// Wide kernel: k-blocks accumulator half 1 trails half 0 (gemm.cuh).  A lag
-// lets one half's epilogue overlap the other half's MMAs but takes ring stages
-// away from the TMA prefetch: 0 for dH (K = V_l, the epilogue is negligible).
-// LCE_WIDE_LAG_<class index> / LCE_WIDE_LAG override.
-constexpr int kWideLagDefault[LCE_K_COUNT] = {1, 1, 1, 1, 1, 0, 1, 1, 1};
-int wide_lag(int cls) {
-  char name[32];
-  snprintf(name, sizeof(name), "LCE_WIDE_LAG_%d", cls);
-  const char* e = getenv(name);
-  if (!e) e = getenv("LCE_WIDE_LAG");
-  return e ? atoi(e) : kWideLagDefault[cls];
-}
-// rows of one output tile (one persistent work unit) of a GEMM class
-int tile_rows(int cls) {
-  if (!use_pair()) return BM;
-  return use_wide(cls, kWideDefault[cls]) ? kWideBM : kPairBM;
-}
 
+// wide_pref: this call site's tile shape (0: 256 x 256 pair tiles, 1: 512 x 256
+// wide tiles); environment overrides win.
 template <bool A_MN, bool B_MN, class Epi>
 lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, const GemmDims& d_in,
-                         const typename Epi::Params& ep, int sms, cudaStream_t s) {
+                         const typename Epi::Params& ep, int sms, cudaStream_t s, int wide_pref = 0) {
   GemmDims d = d_in;
   // dH / dW have few N tiles (N = D) and long K: an N-fastest raster
   // (group_m = 1) lets the concurrently resident tiles of one A row block
@@ -512,8 +511,7 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const bool wide = use_wide(cls, kWideDefault[cls]) != 0;
-  d.wide_lag = wide_lag(cls);
+  const bool wide = use_wide(cls, wide_pref) != 0;
   if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
   cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
                        : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
@@ -810,7 +808,9 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
       EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx, 0, 1};
-      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s)));
+      // pair tiles: this epilogue read-modify-writes the fp32 accumulator rows,
+      // too long to hide behind the wide kernel's single accumulator
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s, 0)));
     }
     // S7 (vocab-parallel): once the last chunk's dH partial is complete, its
     // all-reduce runs on the communicator's side stream while the last dW GEMM
@@ -828,7 +828,8 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
         EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
         ep.use_map = z_tma();
         if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight + v0 * pl.D, pl.D, vc, pl.D));
-        LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+        LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s,
+                                                 pl.cap >= kWideMinRows ? 1 : 0)));
       } else {  // NEXT-2: the AdamW step of these W rows happens in the dW epilogue
         const lce_adamw_t& h = adam->hp;
         const double bc1 = 1.0 - pow(static_cast<double>(h.beta1), static_cast<double>(h.step));
@@ -837,7 +838,9 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
         EpiAdamW::Params ep{adam->theta + o, adam->exp_avg + o, adam->exp_avg_sq + o, adam->w + o, pl.D, hdr,
                             h.lr, h.beta1, h.beta2, h.eps, 1.f - h.lr * h.weight_decay,
                             static_cast<float>(h.lr / bc1), static_cast<float>(sqrt(bc2))};
-        LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s)));
+        // pair tiles: the optimizer epilogue (26 bytes of state traffic per
+        // element) is too long to hide behind the wide kernel's other half
+        LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s, 0)));
       }
     }
   }
@@ -867,7 +870,7 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
     GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
     float* part = split > 1 ? slab : (comm ? vdh : nullptr);
     EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
-    LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s)));
+    LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s, fp.wide_dh)));
   }
   if (split > 1) {
     LaunchScope sc(LCE_K_FINAL, s);
@@ -886,7 +889,7 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
     EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
     ep.use_map = z_tma();
     if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
-    LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s)));
+    LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s, fp.wide_dw)));
   }
   if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
     LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));

@@ -28,8 +28,7 @@ def variant(request, monkeypatch):
     """Every tcgen05 mainloop: the shipped per-class mix (default: 256x256 CTA-pair
     tiles for the forward / recompute GEMMs, 512x256 wide pair tiles for dH / dW),
     CTA pairs everywhere, wide pair tiles everywhere, and the single-CTA kernel."""
-    for k in ("LCE_WIDE", "LCE_WIDE_LAG"):
-        monkeypatch.delenv(k, raising=False)
+    monkeypatch.delenv("LCE_WIDE", raising=False)
     if request.param == "default":
         monkeypatch.delenv("LCE_GEMM", raising=False)
     else:
@@ -546,8 +545,8 @@ def test_fused_matches_recompute_path(cuda_lib):
 # ------------------------------------------------------------ randomized shapes (property test)
 def test_random_shapes_all_paths(cuda_lib):
     """40 seeded random problems (N in [1, 700], D in 8..264 step 8, V in [1, 3000],
-    random ignore fraction, both reductions, every GEMM variant and wide-tile
-    lag, random chunk budgets) through the split and fused paths, each against the oracle."""
+    random ignore fraction, both reductions, every GEMM variant, random chunk
+    budgets) through the split and fused paths, each against the oracle."""
     rng = np.random.default_rng(2024)
     for case in range(40):
         N = int(rng.integers(1, 700))
@@ -556,7 +555,6 @@ def test_random_shapes_all_paths(cuda_lib):
         frac = float(rng.choice([0.0, 0.1, 0.5, 0.95]))
         red = str(rng.choice(["mean", "sum"]))
         os.environ["LCE_GEMM"] = str(rng.choice(["default", "pair", "wide", "single"]))
-        os.environ["LCE_WIDE_LAG"] = str(rng.integers(0, 4))
         try:
             inp = small(N, D, V, seed=100 + case, ignore_frac=frac)
             o = oracle_run(inp, red)
@@ -566,7 +564,6 @@ def test_random_shapes_all_paths(cuda_lib):
             assert_parity(fused_run(inp, red, budget=budget), o, lab)
         finally:
             del os.environ["LCE_GEMM"]
-            del os.environ["LCE_WIDE_LAG"]
 
 
 # ------------------------------------------------------------ NEXT-2: AdamW in the dW epilogue
