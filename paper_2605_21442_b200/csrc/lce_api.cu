@@ -168,6 +168,9 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   int64_t nc_max = (budget / (per_elem * q.ldv)) / kPairBM * kPairBM;
   if (nc_max < kPairBM) nc_max = kPairBM;
   if (nc_max > q.cap) nc_max = q.cap;
+  // at least two row chunks: the chunk buffer never holds all N x V_l
+  // probabilities ("the dense [B, S, V] tensor is never materialized")
+  if (q.cap > kPairBM && nc_max > round_up(ceil_div(q.cap, 2), kPairBM)) nc_max = round_up(ceil_div(q.cap, 2), kPairBM);
   q.n_chunks = ceil_div(q.cap, nc_max);
   q.Nc = round_up(ceil_div(q.cap, q.n_chunks), kPairBM);  // balanced chunks
   // wide tiles pay off once a dW work item's K (= the chunk's rows) is long

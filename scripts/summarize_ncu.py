@@ -63,7 +63,7 @@ def full_metrics(report):
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__cycles_elapsed.avg.per_second", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
-            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed"]
+            "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "sm__cycles_active.avg", "sm__cycles_elapsed.max"]
     res = []
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
@@ -103,9 +103,9 @@ def main():
         print("\n".join(lines))
     if a.report:
         res = full_metrics(a.report)
-        lines = [f"# {a.tag}: ncu --set full ({a.config}), one launch per GEMM kernel", "",
-                 "| kernel | class | duration | DRAM read | DRAM write | tensor pipe active | SM clock | L2 thr. | DRAM thr. | regs |",
-                 "|---|---|---|---|---|---|---|---|---|---|"]
+        lines = [f"# {a.tag}: ncu --set full ({a.config}), one launch per kernel class of one row chunk", "",
+                 "| kernel | class | duration | DRAM read | DRAM write | tensor pipe active | SM active / elapsed cycles | SM clock | L2 thr. | DRAM thr. | regs |",
+                 "|---|---|---|---|---|---|---|---|---|---|---|"]
         tj_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         tj = json.load(open(tj_path)) if os.path.exists(tj_path) else {}
         cfg = tj.setdefault(a.config, {})
@@ -114,6 +114,7 @@ def main():
             short = re.sub(r"\(.*", "", d["kernel"]).replace("void ", "")
             lines.append(f"| `{short}` | {d['class']} | {g('gpu__time_duration.sum')} | {g('dram__bytes_read.sum')} | "
                          f"{g('dram__bytes_write.sum')} | {g('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active')} | "
+                         f"{d.get('sm__cycles_active.avg', ('-',))[0]} / {d.get('sm__cycles_elapsed.max', ('-',))[0]} | "
                          f"{g('sm__cycles_elapsed.avg.per_second')} | {g('lts__throughput.avg.pct_of_peak_sustained_elapsed')} | "
                          f"{g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')} | {g('launch__registers_per_thread')} |")
             if d["class"] and "dram__bytes_read.sum" in d:

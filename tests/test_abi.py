@@ -66,6 +66,16 @@ def test_workspace_formula_bounded(L):
     assert a < b
 
 
+def test_fused_workspace_never_holds_all_logits(L):
+    """the fused path keeps bf16 q/G for one row chunk at a time and
+    always uses at least two chunks, so its workspace stays below the bf16 N x V
+    tensor at every BASELINE shape (and for any chunk budget)."""
+    for (N, D, V) in [(8192, 2048, 128256), (16384, 4096, 128256), (16384, 3584, 152064), (65536, 8192, 128256)]:
+        for budget in (0, 1 << 30, 64 << 30):
+            w = L.lib.lce_fused_workspace_bytes(ctypes.byref(prob(L, N, D, V, budget=budget)))
+            assert 0 < w < N * V * 2, (N, D, V, budget, w)
+
+
 @pytest.mark.parametrize("bad", [
     dict(N=-1), dict(D=0), dict(D=12), dict(V=0), dict(vl=10, vstart=128250), dict(N=1 << 31),
 ])
