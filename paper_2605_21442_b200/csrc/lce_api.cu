@@ -567,6 +567,22 @@ struct lce_comm_s {
 
 namespace {
 
+// SMs a GEMM leaves free while an NCCL collective runs concurrently on the
+// communicator's side stream (vocab-parallel dH all-reduce overlapped with the
+// dW GEMM): the persistent GEMM grid otherwise fills every SM (one
+// CTA per SM, ~227 KB of shared memory each) and the collective's kernel could
+// only start after it.  LCE_VP_RESERVE_SMS overrides (even, 0 = no reservation).
+// (LCE_VP_RESERVE_TEST=1 applies the reservation on a one-rank communicator
+// too, so the reduced-grid launches are covered by the one-GPU tests.)
+int overlap_sms(lce_comm_t comm, int sms) {
+  if (!comm || (comm->nranks < 2 && !getenv("LCE_VP_RESERVE_TEST"))) return sms;
+  const char* e = getenv("LCE_VP_RESERVE_SMS");
+  int r = e ? atoi(e) : 16;
+  r = r < 0 ? 0 : (r > sms / 2 ? sms / 2 : r);
+  return (sms - r) & ~1;
+}
+
+
 lce_status_t allreduce(lce_comm_t c, void* buf, size_t count, ncclRedOp_t op, cudaStream_t s) {
   NcclApi* api = nccl();
   if (!api) return LCE_ERR_NCCL;
@@ -831,7 +847,9 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
         EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
         ep.use_map = z_tma();
         if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight + v0 * pl.D, pl.D, vc, pl.D));
-        LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s,
+        // the last chunk's dW runs beside the dH all-reduce (vocab-parallel)
+        const int g_sms = (multi && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
+        LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, g_sms, s,
                                                  pl.cap >= kWideMinRows ? 1 : 0)));
       } else {  // NEXT-2: the AdamW step of these W rows happens in the dW epilogue
         const lce_adamw_t& h = adam->hp;
@@ -843,7 +861,8 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
                             static_cast<float>(h.lr / bc1), static_cast<float>(sqrt(bc2))};
         // pair tiles: the optimizer epilogue (26 bytes of state traffic per
         // element) is too long to hide behind the wide kernel's other half
-        LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, dev.sms, s, 0)));
+        const int g_sms = (multi && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
+        LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, g_sms, s, 0)));
       }
     }
   }
@@ -892,7 +911,9 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
     EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
     ep.use_map = z_tma();
     if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
-    LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s, fp.wide_dw)));
+    // runs beside this chunk's dH all-reduce under vocab parallelism
+    LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, overlap_sms(comm, sms), s,
+                                            fp.wide_dw)));
   }
   if (comm) {  // cast + scatter the reduced dH rows of the chunk (c already in G)
     LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));

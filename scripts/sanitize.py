@@ -1,5 +1,6 @@
 """Small workload over every entry point for compute-sanitizer (memcheck /
-racecheck / synccheck / initcheck): both GEMM variants, ragged shapes, ignored
+racecheck / synccheck / initcheck): every GEMM variant (256x256 CTA pairs,
+512x256 wide pairs, single CTA), ragged shapes, ignored
 rows, several vocab / row chunks, reduction NONE, the fused path (with and
 without a one-rank communicator), AdamW-in-backward and the KD loss.
 
@@ -20,7 +21,7 @@ from synth.inputs import make_inputs  # noqa: E402
 
 def main():
     comm = F.Comm.single()
-    for variant in ("pair", "single"):
+    for variant in ("pair", "wide", "single"):
         os.environ["LCE_GEMM"] = variant
         for (N, D, V, budget) in [(300, 72, 1000, 0), (130, 64, 513, 300 * 2 * 256)]:
             inp = make_inputs(N, D, V, k=N, device="cuda", ignore_frac=0.2)

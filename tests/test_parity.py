@@ -291,6 +291,28 @@ def test_single_rank_communicator_path(cuda_lib):
         comm.close()
 
 
+@pytest.mark.parametrize("reserve", [16, 38])
+def test_communicator_with_reserved_sms(cuda_lib, monkeypatch, reserve):
+    """Under vocab parallelism the dW GEMM that overlaps the dH all-reduce runs
+    on a reduced persistent grid (SMs left to the collective): the result is
+    unchanged, for the recompute and fused paths, pair and wide tiles."""
+    import paper_2605_21442_b200 as F
+
+    monkeypatch.setenv("LCE_VP_RESERVE_TEST", "1")
+    monkeypatch.setenv("LCE_VP_RESERVE_SMS", str(reserve))
+    comm = F.Comm.single()
+    try:
+        for gemm in ("pair", "wide"):
+            monkeypatch.setenv("LCE_GEMM", gemm)
+            inp = small(1100, 136, 3000, seed=9, ignore_frac=0.2)
+            o = oracle_run(inp)
+            lab = inp.labels.cpu().numpy()
+            assert_parity(gpu_run(inp, comm=comm), o, lab)
+            assert_parity(fused_run(inp, comm=comm, budget=256 * 2 * 3072), o, lab)
+    finally:
+        comm.close()
+
+
 def test_autograd_function(cuda_lib):
     import paper_2605_21442_b200 as F
 
@@ -362,7 +384,7 @@ def test_autograd_none_reduction(cuda_lib):
 
 
 # ------------------------------------------------------------ fused fwd+bwd (no recompute)
-def fused_run(inp, reduction="mean", grad=None, budget=0, accumulate_into=None):
+def fused_run(inp, reduction="mean", grad=None, budget=0, accumulate_into=None, comm=None):
     import paper_2605_21442_b200 as F
 
     g = None
@@ -371,7 +393,7 @@ def fused_run(inp, reduction="mean", grad=None, budget=0, accumulate_into=None):
     dw0 = None if accumulate_into is None else accumulate_into.clone()
     out = F.forward_backward(inp.hidden, inp.weight, inp.labels, grad_loss=g, ignore_index=inp.ignore_index,
                              reduction=reduction, with_token_loss=True, chunk_budget_bytes=budget, dweight=dw0,
-                             accumulate_dweight=accumulate_into is not None)
+                             accumulate_dweight=accumulate_into is not None, comm=comm)
     torch.cuda.synchronize()
     return {
         "loss": out["loss"].item(), "n_valid": int(out["n_valid"].item()),
