@@ -64,6 +64,8 @@ struct GemmDims {
   // L2 eviction priority of the A / B operand loads (0 normal, 1 evict_first,
   // 2 evict_last): operands reused by later tiles of the raster stay in L2
   int32_t a_hint, b_hint;
+  // L2 eviction priority of the epilogue's TMA stores (same encoding)
+  int32_t st_hint;
   // profiler (null = off): CTA 0 records {globaltimer, clock64} at start and
   // end, i.e. the SM clock the kernel actually ran at inside the step
   unsigned long long* probe;
@@ -87,6 +89,7 @@ struct TileInfo {
   int split;      // split-K index of this work item
   uint8_t* smem;  // this warp's kEpiBufs x 4 KB epilogue staging tiles (1 KB aligned)
   uint32_t nst;   // TMA stores this warp has issued so far (selects the next staging tile)
+  uint64_t st_policy;  // L2 cache policy for the epilogue's TMA stores
 };
 
 // This warp's next staging tile: waits (lane 0) until the store that last read
@@ -284,10 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t nst = 0;
+    const uint64_t stp = l2_policy(dims.st_hint);
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
+                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
       Epi::prefetch(ep, ti);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -466,10 +470,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t nst = 0;
+    const uint64_t stp = l2_policy(dims.st_hint);
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
-                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
+                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
       Epi::prefetch(ep, ti);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -680,11 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     uint32_t acc_phase = 0;
     uint32_t nst = 0;
+    const uint64_t stp = l2_policy(dims.st_hint);
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank);
       TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst};
+                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
       Epi::prefetch(ep, ti);
       ti.m0 = m0 + 128;
       Epi::prefetch(ep, ti);

@@ -68,11 +68,13 @@ struct EpiLse : EpiBase {
     fence_async_smem();
     __syncwarp();
     if (l == 0) {
-      tma_store_2d(&p.zmap, st, col, t.m0 + (t.row - l));
+      tma_store_2d_hint(&p.zmap, st, col, t.m0 + (t.row - l), t.st_policy);
       tma_store_commit();
     }
   }
-  template <bool kStoreQ>
+  // kFull: every column of the tile is < n_cols (no per-element bound checks;
+  // same arithmetic and summation order as the checked path)
+  template <bool kStoreQ, bool kFull>
   static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, TileInfo& t, float ml) {
     float s = 0.f;
 #pragma unroll 1
@@ -86,8 +88,8 @@ struct EpiLse : EpiBase {
         const int cb = t.n0 + (2 * c2 + h) * 32;
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
-          const float e0 = cb + j < p.n_cols ? ex2_approx(fmaf(x[j], kLog2e, -ml)) : 0.f;
-          const float e1 = cb + j + 1 < p.n_cols ? ex2_approx(fmaf(x[j + 1], kLog2e, -ml)) : 0.f;
+          const float e0 = (kFull || cb + j < p.n_cols) ? ex2_approx(fmaf(x[j], kLog2e, -ml)) : 0.f;
+          const float e1 = (kFull || cb + j + 1 < p.n_cols) ? ex2_approx(fmaf(x[j + 1], kLog2e, -ml)) : 0.f;
           a0 += e0;
           a1 += e1;
           if (kStoreQ) w[h * 16 + j / 2] = pack_bf16x2(e0, e1);
@@ -140,7 +142,9 @@ struct EpiLse : EpiBase {
       for (int j = 0; j < 32; ++j) m = fmaxf(m, x[j]);
     }
     const float ml = (m == -INFINITY) ? 0.f : m * kLog2e;
-    const float s = p.store_q ? sum_exp<true>(p, taddr, t, ml) : sum_exp<false>(p, taddr, t, ml);
+    const bool full = t.n0 + BN <= p.n_cols;
+    const float s = p.store_q ? (full ? sum_exp<true, true>(p, taddr, t, ml) : sum_exp<true, false>(p, taddr, t, ml))
+                              : (full ? sum_exp<false, true>(p, taddr, t, ml) : sum_exp<false, false>(p, taddr, t, ml));
     if (valid) {
       p.part_m[t.n_blk * p.ld + r] = m;
       p.part_s[t.n_blk * p.ld + r] = s;
@@ -209,7 +213,7 @@ struct EpiG : EpiBase {
         fence_async_smem();
         __syncwarp();
         if (l == 0) {
-          tma_store_2d(&p.gmap, st, t.n0 + c2 * 64, t.m0 + (t.row - l));
+          tma_store_2d_hint(&p.gmap, st, t.n0 + c2 * 64, t.m0 + (t.row - l), t.st_policy);
           tma_store_commit();
         }
       }
@@ -348,9 +352,9 @@ struct EpiDW : EpiBase {
         __syncwarp();
         if (l == 0) {
           if (p.accumulate)
-            tma_reduce_add_2d(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l));
+            tma_reduce_add_2d_hint(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l), t.st_policy);
           else
-            tma_store_2d(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l));
+            tma_store_2d_hint(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l), t.st_policy);
           tma_store_commit();
         }
       }

@@ -496,6 +496,7 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   // 2-12% slower; default normal.)
   d.a_hint = hint_override(cls, 'A', 0);
   d.b_hint = hint_override(cls, 'B', 0);
+  d.st_hint = hint_override(cls, 'S', 0);
   LaunchScope sc(cls, s);
   d.probe = sc.probe();
   if (!use_pair()) {
