@@ -185,6 +185,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk-budget", type=int, default=0,
                     help="chunk_budget_bytes (fused: bf16 q/G chunk bytes, default 2 GiB; split: G chunk, 512 MiB)")
+    ap.add_argument("--parallel", default="vocab", choices=["vocab", "token"],
+                    help="N>1: vocab = W sharded by rows, identical batch on every rank (P:180 loss parallel, the "
+                         "benchmarked mode); token = W replicated, the batch's rows split over ranks, N_v and the loss "
+                         "exchanged by the library and dW all-reduced (the data-parallel gradient reduction)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "split"],
                     help="fused = lce_forward_backward (no logit recompute, 6 N_v V D flops); split = "
                          "lce_forward + lce_backward (recompute from lse, 8 N_v V D flops); auto = fused")
@@ -208,15 +212,20 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-        comm = F.Comm.from_process_group()
+        comm = F.Comm.from_process_group(mode=args.parallel)
     c = CONFIGS[args.config]
     inp = make_config(args.config, device=dev)
     N, D, V = c["N"], c["D"], c["V"]
-    vstart, vl = F.shard_range(V, world, rank) if world > 1 else (0, V)
+    token = world > 1 and args.parallel == "token"
+    vstart, vl = F.shard_range(V, world, rank) if world > 1 and not token else (0, V)
     W = inp.weight[vstart:vstart + vl].contiguous()
     del inp.weight
     H, y = inp.hidden, inp.labels
-    nv = int((y != IGNORE).sum().item())
+    nv = int((y != IGNORE).sum().item())  # non-ignored tokens of the whole (global) batch
+    if token:  # this rank's rows of the global batch (contiguous, the last rank shorter)
+        r0, nr = F.shard_range(N, world, rank)
+        H, y = H[r0:r0 + nr].clone(), y[r0:r0 + nr].clone()
+        N = nr
     ws = F.Workspace()
     stream = torch.cuda.current_stream()
     out = {
@@ -240,6 +249,8 @@ def main():
 
     def step():
         run_path(H, W, y)
+        if token:  # the data-parallel gradient reduction of the replicated head
+            dist.all_reduce(dW)
 
     torch.cuda.reset_peak_memory_stats(dev)
     for _ in range(args.warmup):
@@ -274,9 +285,10 @@ def main():
     tensor_frac = flops_step / (ms_step / 1e3) / (sus * 1e12 * world)
 
     # dominant kernel (by device time inside the timed region, on the launching stream)
-    gemm_flops = {"fwd_gemm": 2.0 * nv * vl * D, "bwd_dh": 2.0 * nv * vl * D, "bwd_dw": 2.0 * nv * vl * D}
+    nv_rank = nv if not token else int((y != IGNORE).sum().item())  # rows this rank projects
+    gemm_flops = {k: 2.0 * nv_rank * vl * D for k in ("fwd_gemm", "bwd_dh", "bwd_dw")}
     if not fused:
-        gemm_flops["bwd_g"] = 2.0 * nv * vl * D  # the recompute GEMM (fused: an HBM-bound fix-up kernel)
+        gemm_flops["bwd_g"] = 2.0 * nv_rank * vl * D  # the recompute GEMM (fused: an HBM-bound fix-up kernel)
     dom = max(prof, key=lambda k: prof[k][0])
     dom_ms, dom_n = prof[dom][:2]
     kernels = {}
@@ -370,14 +382,14 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "N": N, "N_valid": nv, "D": D, "V": V,
-                       "parallelism": f"vocab-parallel x{world}" if world > 1 else "single GPU",
+            "config": {"workload": workload_name(args.config), "N": c["N"], "N_valid": nv, "D": D, "V": V,
+                       "parallelism": f"{args.parallel}-parallel x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (W alone is %.2f GB > 126 MB); no flush" % (V * D * 2 / 1e9)},
             "path": "fused lce_forward_backward" if fused else "lce_forward + lce_backward",
             "flops_per_step": flops_step,
             "tensor_frac": tensor_frac,
             "tensor_frac_note": f"{'6' if fused else '8'}*N_v*V*D executed flops per step / (time x {src} sustained bf16 peak x GPUs)",
-            "peak_hbm_bytes": peak_hbm, "naive_logits_bytes_fp32": N * V * 4,
+            "peak_hbm_bytes": peak_hbm, "naive_logits_bytes_fp32": c["N"] * V * 4,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "clocks": clk, "kernels": kernels,

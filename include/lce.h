@@ -65,8 +65,27 @@ typedef enum {
  * G_ij = g_i (softmax(z_i)_j - [j = y_i]). */
 typedef enum { LCE_MEAN = 0, LCE_SUM = 1, LCE_NONE = 2 } lce_reduction_t;
 
-/* Opaque vocab-parallel communicator (NCCL over NVLink).  NULL = one GPU. */
+/* Opaque communicator (NCCL over NVLink).  NULL = one GPU. */
 typedef struct lce_comm_s* lce_comm_t;
+
+/* How a communicator partitions the problem (north star):
+ *  LCE_PAR_VOCAB (lce_comm_init): W sharded by contiguous row blocks
+ *    (vocab_start, vocab_local); every rank passes the same hidden / labels;
+ *    the row statistics and dH are all-reduced, dW stays local (the rank's
+ *    shard).  loss, lse, dH are the global ones on every rank.
+ *  LCE_PAR_TOKEN (lce_comm_init_mode): W replicated (vocab_local ==
+ *    vocab_total), each rank passes its own rows (N may differ per rank).
+ *    Only two scalars are exchanged: the non-ignored count (MEAN divides by
+ *    the global N_v in the loss and in the gradient scale) and the loss, which
+ *    is the full batch's on every rank.  lse / token_loss / dhidden are the
+ *    rank's own rows; dweight is the rank's contribution, i.e. the sum over
+ *    ranks of dweight is the full batch's dW -- reduce it with the
+ *    data-parallel gradient reduction (e.g. FSDP's reduce-scatter).
+ *    n_valid reports the global N_v.  lce_backward_adamw needs the full dW
+ *    and returns LCE_ERR_COMM with a token-parallel communicator.  Every rank
+ *    must make the same calls (the scalar exchanges are collectives), also a
+ *    rank whose N is 0. */
+typedef enum { LCE_PAR_VOCAB = 0, LCE_PAR_TOKEN = 1 } lce_parallel_t;
 
 typedef struct {
   int64_t n_tokens;      /* N >= 0                                                  */
@@ -210,16 +229,19 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
  * status word, so a fresh (uninitialised) workspace needs no clearing. */
 lce_status_t lce_check_device_status(void* workspace, void* stream);
 
-/* ---- vocab-parallel communicator (P:180 loss parallel) --------------------
+/* ---- communicator (vocab-parallel P:180 loss parallel, or token-parallel) --
  * Rank 0 creates a 128-byte id (host memory) and distributes it out of band
  * (the Python binding uses torch.distributed.broadcast_object_list); every
  * rank then calls lce_comm_init with its own CUDA device current.  NCCL is
  * loaded at run time (libnccl.so.2); LCE_ERR_NCCL if unavailable. */
 lce_status_t lce_comm_get_unique_id(uint8_t id[128]);
 lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank);
+/* lce_comm_init with an explicit lce_parallel_t mode (lce_comm_init = VOCAB). */
+lce_status_t lce_comm_init_mode(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank, int mode);
 lce_status_t lce_comm_destroy(lce_comm_t comm);
 int lce_comm_size(lce_comm_t comm);
 int lce_comm_rank(lce_comm_t comm);
+int lce_comm_mode(lce_comm_t comm); /* lce_parallel_t; LCE_PAR_VOCAB for NULL */
 
 /* ---- introspection ------------------------------------------------------- */
 const char* lce_status_string(lce_status_t s);

@@ -25,6 +25,7 @@ STATUS = {
 EXPORTS = [
     "lce_workspace_bytes", "lce_forward", "lce_backward", "lce_check_device_status",
     "lce_comm_get_unique_id", "lce_comm_init", "lce_comm_destroy", "lce_comm_size", "lce_comm_rank",
+    "lce_comm_init_mode", "lce_comm_mode",
     "lce_status_string", "lce_abi_version", "lce_launch_count", "lce_profile_enable", "lce_profile_read",
     "lce_profile_read_clocks",
     "lce_debug_gemm", "lce_fused_workspace_bytes", "lce_forward_backward", "lce_backward_adamw",
@@ -89,6 +90,10 @@ def _load() -> ctypes.CDLL:
     lib.lce_comm_get_unique_id.restype = ctypes.c_int
     lib.lce_comm_init.argtypes = [P(vp), ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
     lib.lce_comm_init.restype = ctypes.c_int
+    lib.lce_comm_init_mode.argtypes = [P(vp), ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    lib.lce_comm_init_mode.restype = ctypes.c_int
+    lib.lce_comm_mode.argtypes = [vp]
+    lib.lce_comm_mode.restype = ctypes.c_int
     lib.lce_comm_destroy.argtypes = [vp]
     lib.lce_comm_destroy.restype = ctypes.c_int
     lib.lce_comm_size.argtypes = [vp]

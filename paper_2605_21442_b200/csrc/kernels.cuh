@@ -17,6 +17,9 @@ struct Header {
   int32_t n_valid;    // N_v of the last prep
   float c;            // gradient scale: g (sum) or g / N_v (mean), 0 if N_v = 0
   uint32_t counter;   // last-block-done counter for deterministic reductions
+  int32_t mean_div;   // MEAN divisor: N_v, or under token parallelism the global N_v
+  int32_t tp_nv;      // token parallelism: this rank's N_v, then all-reduced (SUM)
+  int32_t tp_bad;     // token parallelism: out-of-range labels anywhere (all-reduced)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -585,7 +588,21 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
     // MEAN: g / N_v, SUM: g, NONE: 1 (per-token upstream grads are folded into G)
     hdr->c = nv == 0 ? 0.f : (reduction == 0 ? g / static_cast<float>(nv) : (reduction == 1 ? g : 1.f));
     hdr->counter = 0u;
+    hdr->mean_div = nv;
+    hdr->tp_nv = nv;
+    hdr->tp_bad = any_bad ? 1 : 0;
   }
+}
+
+// Token parallelism (rows sharded over ranks, W replicated): after the
+// all-reduce of (tp_nv, tp_bad), MEAN divides by the global N_v -- in the
+// gradient scale c and in the loss -- so the per-rank losses and gradients sum
+// to the full batch's.
+__global__ void tp_scale_kernel(Header* hdr, const float* __restrict__ grad_loss, int reduction) {
+  const int nv = hdr->tp_nv;
+  const float g = (grad_loss && reduction != 2) ? *grad_loss : 1.f;
+  hdr->mean_div = nv;
+  if (hdr->n_valid > 0 && reduction == 0) hdr->c = nv == 0 ? 0.f : g / static_cast<float>(nv);
 }
 
 // ============================================================ S0 gather
@@ -682,10 +699,11 @@ __device__ __forceinline__ void block_loss_reduce(double li, double* block_sums,
     }
     if (threadIdx.x == 0) {
       double L = red[0];
-      if (reduction == 0) L = nv > 0 ? L / nv : 0.0;
+      const int nd = hdr->mean_div;
+      if (reduction == 0) L = nd > 0 ? L / nd : 0.0;
       if (hdr->status & kStatusBadLabel) L = __longlong_as_double(0x7ff8000000000000ULL);
       *loss = static_cast<float>(L);
-      if (n_valid_out) *n_valid_out = nv;
+      if (n_valid_out) *n_valid_out = nd;
       hdr->counter = 0u;
     }
   }
@@ -1022,10 +1040,11 @@ __global__ void __launch_bounds__(1024) loss_reduce_kernel(const float* __restri
   }
   if (threadIdx.x == 0) {
     double L = red[0];
-    if (reduction == 0) L = nv > 0 ? L / nv : 0.0;
+    const int nd = hdr->mean_div;
+    if (reduction == 0) L = nd > 0 ? L / nd : 0.0;
     if (hdr->status & kStatusBadLabel) L = __longlong_as_double(0x7ff8000000000000ULL);
     *loss = static_cast<float>(L);
-    if (n_valid_out) *n_valid_out = nv;
+    if (n_valid_out) *n_valid_out = nd;
   }
 }
 

@@ -37,6 +37,12 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
     }                                                                                    \
   } while (0)
 
+#define LCE_TRY(expr)                  \
+  do {                                 \
+    lce_status_t st_ = (expr);         \
+    if (st_ != LCE_OK) return st_;     \
+  } while (0)
+
 // ------------------------------------------------------------------ workspace plan
 struct Plan {
   int64_t N, D, Vl, cap, n_tiles, Vc, n_chunks, nblocks;
@@ -562,6 +568,7 @@ NcclApi* nccl() {
 struct lce_comm_s {
   ncclComm_t comm;
   int nranks, rank;
+  int mode;  // lce_parallel_t
   cudaStream_t side;          // runs the dH all-reduce concurrently with the last dW GEMM
   cudaEvent_t dh_ready, dh_reduced;
 };
@@ -592,6 +599,50 @@ lce_status_t allreduce(lce_comm_t c, void* buf, size_t count, ncclRedOp_t op, cu
   return LCE_OK;
 }
 
+lce_status_t allreduce_i32(lce_comm_t c, void* buf, size_t count, cudaStream_t s) {
+  NcclApi* api = nccl();
+  if (!api) return LCE_ERR_NCCL;
+  LaunchScope sc(LCE_K_COMM, s);
+  if (api->allReduce(buf, buf, count, ncclInt32, ncclSum, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+  return LCE_OK;
+}
+
+// The vocab-parallel / token-parallel communicator behind `c` (null if none).
+lce_comm_t vocab_comm(lce_comm_t c) { return (c && c->mode == LCE_PAR_VOCAB) ? c : nullptr; }
+lce_comm_t token_comm(lce_comm_t c) { return (c && c->mode == LCE_PAR_TOKEN) ? c : nullptr; }
+
+// Token parallelism, after prep: all-reduce (N_v, bad-label flag) and rescale
+// the MEAN divisor / gradient scale to the global N_v.
+lce_status_t tp_sync(lce_comm_t tp, Header* hdr, const float* grad_loss, int reduction, cudaStream_t s) {
+  if (!tp) return LCE_OK;
+  LCE_TRY(allreduce_i32(tp, &hdr->tp_nv, 2, s));
+  LaunchScope sc(LCE_K_PREP, s);
+  tp_scale_kernel<<<1, 1, 0, s>>>(hdr, grad_loss, reduction);
+  return last_error();
+}
+// Token parallelism: the rank's loss share (sum_i loss_i / N_v_global for
+// MEAN, sum_i loss_i otherwise) summed over ranks.
+lce_status_t tp_loss(lce_comm_t tp, float* loss, cudaStream_t s) {
+  return tp ? allreduce(tp, loss, 1, ncclSum, s) : LCE_OK;
+}
+// Token parallelism, a rank with no tokens: still joins both exchanges.
+lce_status_t tp_empty_rank(lce_comm_t tp, const lce_problem_t* p, Header* hdr, const float* grad_loss,
+                           float* loss, int32_t* n_valid, cudaStream_t s) {
+  {
+    LaunchScope sc(LCE_K_PREP, s);
+    prep_kernel<<<1, 1024, 0, s>>>(nullptr, 0, p->ignore_index, p->vocab_total, nullptr, nullptr, nullptr, nullptr,
+                                   nullptr, hdr, grad_loss, p->reduction);
+    LCE_TRY(last_error());
+  }
+  LCE_TRY(tp_sync(tp, hdr, grad_loss, p->reduction, s));
+  if (loss) {
+    LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
+    LCE_TRY(tp_loss(tp, loss, s));
+  }
+  if (n_valid) LCE_CUDA(cudaMemcpyAsync(n_valid, &hdr->mean_div, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  return LCE_OK;
+}
+
 lce_status_t validate(const lce_problem_t* p, lce_comm_t comm, size_t ws_bytes, const void* ws, Plan* pl) {
   if (!p) return LCE_ERR_NULL;
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
@@ -599,15 +650,10 @@ lce_status_t validate(const lce_problem_t* p, lce_comm_t comm, size_t ws_bytes, 
   if (!ws) return LCE_ERR_NULL;
   if (!aligned16(ws)) return LCE_ERR_ALIGN;
   if (ws_bytes < pl->total) return LCE_ERR_WORKSPACE;
-  if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
+  if (!vocab_comm(comm) && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
   return LCE_OK;
 }
 
-#define LCE_TRY(expr)                  \
-  do {                                 \
-    lce_status_t st_ = (expr);         \
-    if (st_ != LCE_OK) return st_;     \
-  } while (0)
 
 }  // namespace
 
@@ -641,11 +687,12 @@ size_t lce_workspace_bytes(const lce_problem_t* p) {
   return pl.total;
 }
 
-lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden, const uint16_t* weight,
                          const int32_t* labels, float* loss, float* lse, float* token_loss, int32_t* n_valid,
                          void* workspace, size_t workspace_bytes, void* stream) {
   Plan pl;
-  LCE_TRY(validate(p, comm, workspace_bytes, workspace, &pl));
+  LCE_TRY(validate(p, comm_in, workspace_bytes, workspace, &pl));
+  lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
   if (!weight || !loss) return LCE_ERR_NULL;
   if (pl.N > 0 && (!hidden || !labels || !lse)) return LCE_ERR_NULL;
   const void* ptrs[] = {hidden, weight, labels, loss, lse, token_loss, n_valid};
@@ -658,6 +705,7 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
   Header* hdr = reinterpret_cast<Header*>(ws + pl.hdr);
 
   if (pl.N == 0) {  // empty batch: loss 0, N_v 0, nothing to project
+    if (tp) return tp_empty_rank(tp, p, hdr, nullptr, loss, n_valid, s);
     LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
     if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
     return LCE_OK;
@@ -680,6 +728,7 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
                                    nullptr, p->reduction);
     LCE_TRY(last_error());
   }
+  LCE_TRY(tp_sync(tp, hdr, nullptr, p->reduction, s));
   {  // S0: gather valid rows of H
     LaunchScope sc(LCE_K_GATHER, s);
     gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, nullptr, nullptr,
@@ -701,7 +750,8 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm, const uint16_t
     LaunchScope sc(LCE_K_COMBINE, s);
     combine_kernel<<<cblocks, 256, 0, s>>>(0, pm, ps, nt, pl.cap, mloc, mglob, sbuf, zt, idx, hdr, lse, token_loss,
                                            bsum, loss, n_valid, p->reduction);
-    return last_error();
+    LCE_TRY(last_error());
+    return tp_loss(tp, loss, s);
   }
   {  // with a communicator (any size, including 1): local merge first
     LaunchScope sc(LCE_K_COMBINE, s);
@@ -743,12 +793,14 @@ struct AdamArgs {
   lce_adamw_t hp;
 };
 
-lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
+lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden, const uint16_t* weight,
                            const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
                            float* dweight, int accumulate_dweight, const AdamArgs* adam, void* workspace,
                            size_t workspace_bytes, void* stream) {
   Plan pl;
-  LCE_TRY(validate(p, comm, workspace_bytes, workspace, &pl));
+  LCE_TRY(validate(p, comm_in, workspace_bytes, workspace, &pl));
+  lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
+  if (tp && adam) return LCE_ERR_COMM;  // the in-backward step needs the full-batch dW
   if (!weight || (!dweight && !adam)) return LCE_ERR_NULL;
   if (pl.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
   const void* ptrs[] = {hidden, weight, labels, lse, grad_loss, dhidden, dweight};
@@ -762,6 +814,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
 
   if (pl.N == 0 && !adam) {
     if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, pl.Vl * pl.D * sizeof(float), s));
+    if (tp) return tp_empty_rank(tp, p, hdr, grad_loss, nullptr, nullptr, s);
     return LCE_OK;
   }
   if (pl.N == 0) {  // empty batch, in-backward AdamW: the step still runs with g = 0
@@ -796,6 +849,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm, const uint16
                                    grad_loss, p->reduction);
     LCE_TRY(last_error());
   }
+  LCE_TRY(tp_sync(tp, hdr, grad_loss, p->reduction, s));
   {
     LaunchScope sc(LCE_K_GATHER, s);
     gather_kernel<<<static_cast<unsigned>(pl.cap), 128, 0, s>>>(hidden, pl.D, N, idx, hdr, hc, lse, lsec, row_grad,
@@ -958,7 +1012,7 @@ size_t lce_fused_workspace_bytes(const lce_problem_t* p) {
   return fp.total;
 }
 
-lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden,
+lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden,
                                   const uint16_t* weight, const int32_t* labels, const float* grad_loss,
                                   float* loss, float* lse, float* token_loss, int32_t* n_valid, uint16_t* dhidden,
                                   float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
@@ -967,6 +1021,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   FusedPlan fp;
   if (!make_fused_plan(p, &fp)) return LCE_ERR_SHAPE;
+  lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
   if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
   if (!workspace || !weight || !loss || !dweight) return LCE_ERR_NULL;
   if (fp.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
@@ -980,9 +1035,10 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
   if (fp.N == 0) {
+    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, fp.Vl * fp.D * sizeof(float), s));
+    if (tp) return tp_empty_rank(tp, p, hdr, grad_loss, loss, n_valid, s);
     LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
     if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
-    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, fp.Vl * fp.D * sizeof(float), s));
     return LCE_OK;
   }
   const int N = static_cast<int>(fp.N);
@@ -1009,6 +1065,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
                                    grad_loss, p->reduction);
     LCE_TRY(last_error());
   }
+  LCE_TRY(tp_sync(tp, hdr, grad_loss, p->reduction, s));
   {
     LaunchScope sc(LCE_K_GATHER, s);
     gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden, fp.D, N, idx, hdr, hc, nullptr, nullptr,
@@ -1080,7 +1137,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm, const
     loss_reduce_kernel<<<1, 1024, 0, s>>>(ltok, hdr, loss, n_valid, p->reduction);
     LCE_TRY(last_error());
   }
-  return LCE_OK;
+  return tp_loss(tp, loss, s);
 }
 
 size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim) {
@@ -1089,7 +1146,7 @@ size_t lce_kd_workspace_bytes(const lce_problem_t* p, int64_t teacher_dim) {
   return kp.total;
 }
 
-lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, int64_t teacher_dim,
+lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, int64_t teacher_dim,
                                      const uint16_t* hidden_s, const uint16_t* weight_s, const uint16_t* hidden_t,
                                      const uint16_t* weight_t, const int32_t* labels, const float* grad_loss,
                                      float* loss, float* token_loss, int32_t* n_valid, uint16_t* dhidden_s,
@@ -1099,6 +1156,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   KdPlan kp;
   if (!make_kd_plan(p, teacher_dim, &kp)) return LCE_ERR_SHAPE;
+  lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
   if (!comm && (p->vocab_start != 0 || p->vocab_local != p->vocab_total)) return LCE_ERR_COMM;
   const FusedPlan& fp = kp.f;
   if (!workspace || !weight_s || !weight_t || !loss || !dweight_s) return LCE_ERR_NULL;
@@ -1114,9 +1172,10 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
   if (fp.N == 0) {
+    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight_s, 0, fp.Vl * fp.D * sizeof(float), s));
+    if (tp) return tp_empty_rank(tp, p, hdr, grad_loss, loss, n_valid, s);
     LCE_CUDA(cudaMemsetAsync(loss, 0, sizeof(float), s));
     if (n_valid) LCE_CUDA(cudaMemsetAsync(n_valid, 0, sizeof(int32_t), s));
-    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight_s, 0, fp.Vl * fp.D * sizeof(float), s));
     return LCE_OK;
   }
   const int N = static_cast<int>(fp.N);
@@ -1149,6 +1208,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
                                    grad_loss, p->reduction);
     LCE_TRY(last_error());
   }
+  LCE_TRY(tp_sync(tp, hdr, grad_loss, p->reduction, s));
   {
     LaunchScope sc(LCE_K_GATHER, s);
     gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden_s, fp.D, N, idx, hdr, hcs, nullptr, nullptr,
@@ -1237,7 +1297,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
     loss_reduce_kernel<<<1, 1024, 0, s>>>(ltok, hdr, loss, n_valid, p->reduction);
     LCE_TRY(last_error());
   }
-  return LCE_OK;
+  return tp_loss(tp, loss, s);
 }
 
 lce_status_t lce_check_device_status(void* workspace, void* stream) {
@@ -1261,7 +1321,8 @@ lce_status_t lce_comm_get_unique_id(uint8_t id[128]) {
   return LCE_OK;
 }
 
-lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank) {
+lce_status_t lce_comm_init_mode(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank, int mode) {
+  if (mode != LCE_PAR_VOCAB && mode != LCE_PAR_TOKEN) return LCE_ERR_COMM;
   if (!comm || !id) return LCE_ERR_NULL;
   if (nranks < 1 || rank < 0 || rank >= nranks) return LCE_ERR_SHAPE;
   NcclApi* api = nccl();
@@ -1270,7 +1331,7 @@ lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, 
   memcpy(&u, id, 128);
   ncclComm_t c;
   if (api->commInitRank(&c, nranks, u, rank) != ncclSuccess) return LCE_ERR_NCCL;
-  lce_comm_s* cs = new lce_comm_s{c, nranks, rank, nullptr, nullptr, nullptr};
+  lce_comm_s* cs = new lce_comm_s{c, nranks, rank, mode, nullptr, nullptr, nullptr};
   if (cudaStreamCreateWithFlags(&cs->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&cs->dh_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&cs->dh_reduced, cudaEventDisableTiming) != cudaSuccess) {
@@ -1280,6 +1341,10 @@ lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, 
   }
   *comm = cs;
   return LCE_OK;
+}
+
+lce_status_t lce_comm_init(lce_comm_t* comm, const uint8_t id[128], int nranks, int rank) {
+  return lce_comm_init_mode(comm, id, nranks, rank, LCE_PAR_VOCAB);
 }
 
 lce_status_t lce_comm_destroy(lce_comm_t comm) {
@@ -1296,6 +1361,7 @@ lce_status_t lce_comm_destroy(lce_comm_t comm) {
 
 int lce_comm_size(lce_comm_t comm) { return comm ? comm->nranks : 1; }
 int lce_comm_rank(lce_comm_t comm) { return comm ? comm->rank : 0; }
+int lce_comm_mode(lce_comm_t comm) { return comm ? comm->mode : LCE_PAR_VOCAB; }
 
 lce_status_t lce_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);

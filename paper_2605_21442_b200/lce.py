@@ -78,16 +78,24 @@ def _check_inputs(hidden, weight, labels):
             raise ValueError("tensors must be contiguous CUDA tensors")
 
 
-class Comm:
-    """Vocab-parallel communicator (NCCL over NVLink) owned by the library."""
+PARALLEL_MODES = {"vocab": 0, "token": 1}  # lce_parallel_t
 
-    def __init__(self, handle: ctypes.c_void_p, world: int, rank: int):
+
+class Comm:
+    """Communicator (NCCL over NVLink) owned by the library.
+
+    mode "vocab" (P:180 loss parallel): W sharded by rows, identical hidden /
+    labels on every rank.  mode "token": W replicated, each rank its own rows;
+    MEAN uses the global N_v and dweight is the rank's share (include/lce.h)."""
+
+    def __init__(self, handle: ctypes.c_void_p, world: int, rank: int, mode: str = "vocab"):
         self.handle = handle
         self.world = world
         self.rank = rank
+        self.mode = mode
 
     @classmethod
-    def from_process_group(cls, group=None) -> "Comm":
+    def from_process_group(cls, group=None, mode: str = "vocab") -> "Comm":
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
@@ -98,17 +106,18 @@ class Comm:
             payload = bytes(buf.raw)
         uid = broadcast_bytes(payload, group=group)
         h = ctypes.c_void_p()
-        check(lib.lce_comm_init(ctypes.byref(h), uid, world, rank), "lce_comm_init")
-        return cls(h, world, rank)
+        check(lib.lce_comm_init_mode(ctypes.byref(h), uid, world, rank, PARALLEL_MODES[mode]), "lce_comm_init_mode")
+        return cls(h, world, rank, mode)
 
     @classmethod
-    def single(cls) -> "Comm":
+    def single(cls, mode: str = "vocab") -> "Comm":
         """A one-rank communicator: exercises the exchange path on one GPU."""
         buf = ctypes.create_string_buffer(128)
         check(lib.lce_comm_get_unique_id(buf), "lce_comm_get_unique_id")
         h = ctypes.c_void_p()
-        check(lib.lce_comm_init(ctypes.byref(h), bytes(buf.raw), 1, 0), "lce_comm_init")
-        return cls(h, 1, 0)
+        check(lib.lce_comm_init_mode(ctypes.byref(h), bytes(buf.raw), 1, 0, PARALLEL_MODES[mode]),
+              "lce_comm_init_mode")
+        return cls(h, 1, 0, mode)
 
     def close(self):
         if self.handle:

@@ -1,7 +1,9 @@
 """Multi-process (gloo, CPU) tests of the vocab-parallel path's host logic and
 of the exchange protocol the CUDA path implements (P:169, P:180 loss parallel):
 all-reduce MAX of the per-row shard max, rescale, all-reduce SUM of
-(sum-exp, target logit), then all-reduce SUM of the partial dH."""
+(sum-exp, target logit), then all-reduce SUM of the partial dH.  And the
+token-parallel protocol (W replicated, rows sharded): all-reduce SUM of N_v,
+each rank's MEAN share with the global N_v, loss and dW summed over ranks."""
 
 import math
 import os
@@ -91,6 +93,45 @@ def _worker_protocol(rank, world, port, reduction):
     np.testing.assert_allclose(full.numpy(), gref["dW"], rtol=1e-11, atol=1e-14)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def _worker_token_protocol(rank, world, port, reduction):
+    """Rows sharded unevenly over ranks (rank 0 may hold none): the library's
+    LCE_PAR_TOKEN exchange -- N_v all-reduced, MEAN divides by the global N_v
+    in the loss and in the gradient scale, loss all-reduced, dW the rank's
+    share -- reproduces the full batch."""
+    _init(rank, world, port)
+    H, W, y = _problem()
+    N = len(y)
+    bounds = [0] + sorted(np.random.default_rng(world).integers(0, N + 1, size=world - 1).tolist()) + [N]
+    bounds[1] = 0 if world > 2 else bounds[1]  # rank 0 without tokens when there are >= 3 ranks
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    Hr, yr = H[r0:r1], y[r0:r1]
+    nv = torch.tensor([int(((yr != IGNORE_INDEX) & (yr >= 0)).sum())], dtype=torch.int64)
+    dist.all_reduce(nv, op=dist.ReduceOp.SUM)
+    nv = int(nv.item())
+    f = lce_forward(Hr, W, yr, reduction="sum") if r1 > r0 else {"loss": 0.0}
+    loss = torch.tensor([f["loss"] / nv if reduction == "mean" else f["loss"]], dtype=torch.float64)
+    dist.all_reduce(loss, op=dist.ReduceOp.SUM)
+    ref = lce_forward(H, W, y, reduction=reduction)
+    assert loss.item() == pytest.approx(ref["loss"], rel=1e-12)
+    g = 1.0 / nv if reduction == "mean" else 1.0
+    if r1 > r0:
+        b = lce_backward(Hr, W, yr, reduction="sum", grad_loss=g)
+        dw, dh = torch.tensor(b["dW"]), b["dH"]
+    else:
+        dw, dh = torch.zeros(W.shape, dtype=torch.float64), np.zeros((0, W.shape[1]))
+    dist.all_reduce(dw, op=dist.ReduceOp.SUM)
+    gref = lce_backward(H, W, y, reduction=reduction)
+    np.testing.assert_allclose(dw.numpy(), gref["dW"], rtol=1e-11, atol=1e-14)
+    np.testing.assert_allclose(dh, gref["dH"][r0:r1], rtol=1e-11, atol=1e-14)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,reduction", [(2, "mean"), (3, "mean"), (3, "sum")])
+def test_gloo_token_parallel_protocol(world, reduction):
+    mp.spawn(_worker_token_protocol, args=(world, free_port(), reduction), nprocs=world, join=True)
 
 
 @pytest.mark.parametrize("V,P", [(128256, 8), (152064, 8), (1000, 3), (101, 2), (7, 8), (5, 1)])

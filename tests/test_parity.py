@@ -16,7 +16,7 @@ import pytest
 import torch
 
 from oracle import lce_backward, lce_forward, lce_rows
-from synth.inputs import CONFIGS, IGNORE, make_config, make_inputs, packed_labels
+from synth.inputs import CONFIGS, IGNORE, LceInputs, make_config, make_inputs, packed_labels
 
 pytestmark = pytest.mark.gpu
 
@@ -311,6 +311,65 @@ def test_communicator_with_reserved_sms(cuda_lib, monkeypatch, reserve):
             assert_parity(fused_run(inp, comm=comm, budget=256 * 2 * 3072), o, lab)
     finally:
         comm.close()
+
+
+def test_token_parallel_communicator_one_rank(cuda_lib):
+    """LCE_PAR_TOKEN on one rank is the single-GPU problem: forward / backward,
+    fused and KD match the oracle through the token-parallel code path (the
+    N_v and loss exchanges); the in-backward AdamW refuses it (needs the full
+    dW); a rank with no tokens still completes its exchanges."""
+    import paper_2605_21442_b200 as F
+    comm = F.Comm.single("token")
+    try:
+        assert F.lib.lce_comm_mode(comm.handle) == 1
+        inp = small(700, 136, 3000, seed=21, ignore_frac=0.3)
+        lab = inp.labels.cpu().numpy()
+        for red in ("mean", "sum"):
+            o = oracle_run(inp, red)
+            assert_parity(gpu_run(inp, red, comm=comm), o, lab)
+            assert_parity(fused_run(inp, red, comm=comm, budget=256 * 2 * 3072), o, lab)
+        t = make_inputs(700, 72, 3000, k=22, device="cuda", label_override=lab)
+        kd = F.kd_forward_backward(inp.hidden, inp.weight, t.hidden, t.weight, inp.labels, comm=comm)
+        kd0 = F.kd_forward_backward(inp.hidden, inp.weight, t.hidden, t.weight, inp.labels)
+        assert abs(kd["loss"].item() - kd0["loss"].item()) <= 1e-6 * abs(kd0["loss"].item())
+        assert torch.equal(kd["dhidden"], kd0["dhidden"])
+        theta = inp.weight.float().clone()
+        with pytest.raises(F.LceError):
+            F.backward_adamw(inp.hidden, inp.weight.clone(), inp.labels, torch.zeros(700, device="cuda"), theta,
+                             torch.zeros_like(theta), torch.zeros_like(theta), lr=1e-3, step=1, comm=comm)
+        e = small(0, 64, 1000, seed=23)
+        out = F.forward_backward(e.hidden, e.weight, e.labels, comm=comm)
+        torch.cuda.synchronize()
+        assert out["loss"].item() == 0.0 and int(out["n_valid"].item()) == 0
+        assert torch.count_nonzero(out["dweight"]).item() == 0
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("path", ["split", "fused"])
+def test_token_parallel_decomposition(cuda_lib, path):
+    """What each token-parallel rank computes, checked on one GPU through the
+    public API: rows split unevenly into shards, each shard with reduction SUM
+    and upstream gradient 1 / N_v(global) (the scale LCE_PAR_TOKEN applies to
+    MEAN) -- the shard losses and dW shares sum to, and the dH rows
+    concatenate to, the full batch's MEAN result."""
+    inp = small(1100, 136, 3000, seed=24, ignore_frac=0.25)
+    lab = inp.labels.cpu().numpy()
+    o = oracle_run(inp, "mean")
+    nv = int((lab != IGNORE).sum())
+    cuts = [0, 0, 313, 1100]  # the first shard holds no tokens
+    loss, dW, dH, tok = 0.0, 0.0, [], []
+    for a, b in zip(cuts, cuts[1:]):
+        part = LceInputs(hidden=inp.hidden[a:b].clone(), weight=inp.weight, labels=inp.labels[a:b].clone())
+        g = gpu_run(part, "sum", grad=1.0 / nv) if path == "split" else fused_run(part, "sum", grad=1.0 / nv)
+        loss += g["loss"] / nv
+        dW = dW + g["dW"]
+        dH.append(g["dH"])
+        tok.append(g["tok"])
+    assert abs(loss - o["loss"]) <= LOSS_TOL * abs(o["loss"])
+    assert fro_rel(np.concatenate(dH), o["dH"]) <= GRAD_TOL
+    assert fro_rel(dW, o["dW"]) <= GRAD_TOL
+    assert np.abs(np.concatenate(tok) - o["tok"]).max() <= LSE_TOL * max(1.0, np.abs(o["lse"]).max())
 
 
 def test_autograd_function(cuda_lib):
