@@ -327,7 +327,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Epilogues are unchanged: each CTA drains its own 128 TMEM lanes.
 // =====================================================================
 constexpr int kPairBM = 256;  // rows per pair tile
-constexpr int kPairStages = 6;
+#ifndef LCE_PAIR_STAGES
+#define LCE_PAIR_STAGES 6
+#endif
+constexpr int kPairStages = LCE_PAIR_STAGES;
 constexpr int kPairStageBytes = 128 * BK * 2 * 2;  // A half + B half = 32 KB
 constexpr int kPairSmemBytes = kPairStages * kPairStageBytes + 1024 + 1024 + kEpiSmemBytes;
 
