@@ -174,7 +174,7 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
                                 void* workspace, size_t workspace_bytes,
                                 void* stream);
 
-/* ---- fused forward + backward (one GPU) ------------------------------------
+/* ---- fused forward + backward ----------------------------------------------
  * The same results as lce_forward followed by lce_backward (loss, lse,
  * token_loss, n_valid, dhidden, dweight; same argument meanings), computed
  * without recomputing the logits: P:166's "processes hidden states in
@@ -185,10 +185,13 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
  * place and consumed by the dH and dW GEMMs: 6 N_v V D flops instead of 8.
  * The upstream gradient must be known up front (grad_loss as in lce_backward;
  * NULL = 1).  dW is accumulated across row chunks in fp32.  Nc is set by
- * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB).  With comm != NULL (vocab-parallel,
- * P:180) each row chunk's (max, sum-exp, target logit) are combined with the
- * same MAX / SUM all-reduces as lce_forward, and the chunk's fp32 dH partial is
- * all-reduced on the communicator's side stream while the dW GEMM runs. */
+ * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB) and is at
+ * most half the rows, so the buffer never holds all N x V_l probabilities.
+ * With a vocab-parallel comm each row chunk's (max, sum-exp, target
+ * logit) are combined with the same MAX / SUM all-reduces as lce_forward, and
+ * the chunk's fp32 dH partial is all-reduced on the communicator's side stream
+ * while the dW GEMM runs (on SMs left free for it).  With a token-parallel
+ * comm see lce_parallel_t. */
 size_t lce_fused_workspace_bytes(const lce_problem_t* p);
 lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
                                   const uint16_t* hidden, const uint16_t* weight,
