@@ -250,17 +250,48 @@ struct EpiDH : EpiBase {
     int32_t use_c;         // 1: scale by c on output; 0: c already folded into G
     float* part;           // split-K: fp32 partial slabs [ksplit][rows][ld] (reduced by reduce_dh_kernel)
     int64_t part_stride;   // elements per slab
+    int32_t use_map;       // 1: accumulate into acc_buf through `map` with TMA stores (first chunk) /
+                           //    TMA reduce-adds (the L2 adds; no read by the SM); unscaled, a
+                           //    finalize pass applies c, rounds and scatters
+    alignas(64) CUtensorMap map;  // acc_buf [rows, ld] fp32, 32 x 32 boxes, 128B swizzle
   };
   // pull the running fp32 sum of this tile's row into L2 while the MMA runs
   static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
     const int r = t.m0 + t.row;
-    if (p.part || p.first || r >= t.M) return;
+    if (p.part || p.first || p.use_map || r >= t.M) return;
     const float* row = p.acc_buf + static_cast<int64_t>(p.row_off + r) * p.ld;
     for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
   }
-  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
+  static __device__ __forceinline__ void finish(const Params& p) {
+    if (p.use_map && (threadIdx.x & 31) == 0) tma_store_wait_all();
+  }
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
+    if (p.use_map && !p.part) {  // TMA store / reduce-add of the unscaled chunk sum
+      const int l = t.row & 31;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float x[32];
+        load_chunk(taddr, c, t.zero_acc, x);
+        if (t.n0 + c * 32 >= t.N) continue;  // uniform across the warp
+        uint8_t* st = stage_next(t);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
+              make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (l == 0) {
+          if (p.first)
+            tma_store_2d_hint(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l), t.st_policy);
+          else
+            tma_reduce_add_2d_hint(&p.map, st, t.n0 + c * 32, t.m0 + (t.row - l), t.st_policy);
+          tma_store_commit();
+        }
+      }
+      return;
+    }
     if (p.part) {  // split-K partial: plain fp32 store, no read-modify-write
       float* prow = p.part + t.split * p.part_stride + static_cast<int64_t>(r) * p.ld;
 #pragma unroll 1

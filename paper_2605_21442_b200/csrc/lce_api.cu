@@ -842,6 +842,10 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
   uint16_t* G = reinterpret_cast<uint16_t*>(ws + pl.g);
   float* dh = reinterpret_cast<float*>(ws + pl.dh);
   const bool multi = comm && comm->nranks >= 1;
+  // dH chunks accumulate through TMA stores / reduce-adds (then one finalize
+  // pass) instead of an SM read-modify-write per chunk; LCE_DH_TMA=0 selects
+  // the read-modify-write epilogue (A/B)
+  const bool dh_tma = z_tma() && !(getenv("LCE_DH_TMA") && atoi(getenv("LCE_DH_TMA")) == 0);
 
   {
     LaunchScope sc(LCE_K_PREP, s);
@@ -881,10 +885,14 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
     // S6: dH (+)= G_c W_c   (A = G_c K-major over vocab, B = W_c MN-major)
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
-      EpiDH::Params ep{dh, pl.D, k == 0, (!multi && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx, 0, 1};
-      // pair tiles: this epilogue read-modify-writes the fp32 accumulator rows,
-      // too long to hide behind the wide kernel's single accumulator
-      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s, 0)));
+      EpiDH::Params ep{dh, pl.D, k == 0, (!multi && !dh_tma && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx,
+                       0, 1};
+      ep.use_map = dh_tma ? 1 : 0;
+      if (dh_tma) LCE_TRY(map_f32_store(&ep.map, dh, pl.D, pl.cap, pl.D));
+      // the TMA epilogue is short enough for wide tiles; the read-modify-write
+      // one (LCE_DH_TMA=0) is not
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s,
+                                               (dh_tma && pl.cap >= kWideMinRows) ? 1 : 0)));
     }
     // S7 (vocab-parallel): once the last chunk's dH partial is complete, its
     // all-reduce runs on the communicator's side stream while the last dW GEMM
@@ -921,9 +929,9 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
       }
     }
   }
-  if (multi) {
+  if (multi || dh_tma) {
     // S7: dH summed over the vocab shards, then scaled, cast, scattered
-    LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
+    if (multi) LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
     LaunchScope sc(LCE_K_FINAL, s);
     finalize_dh_kernel<<<static_cast<unsigned>(pl.N), 256, 0, s>>>(dh, pl.D, idx, hdr, dhidden);
     LCE_TRY(last_error());
