@@ -573,6 +573,46 @@ def test_vocab_shard_offsets_single_rank(cuda_lib, path):
     assert fro_rel(dw.cpu().double().numpy(), sb["dW_shard"]) <= GRAD_TOL
 
 
+def test_vocab_shard_full_size_p8_rank(cuda_lib):
+    """The per-rank workload of the 8-GPU vocab-parallel 8B run on one GPU:
+    rank 2's shard of W (V_l = 16,032 rows, not a tile multiple) at N = 16,384,
+    D = 4,096 through the fused path on a one-rank communicator, so the 8,192-row
+    chunks take the wide dH / dW tiles over a ragged vocab extent.  lse / token
+    loss of 256 sampled rows and the full dW shard against the oracle's shard
+    statistics (evaluated in row blocks)."""
+    import paper_2605_21442_b200 as F
+    from oracle import shard_backward, shard_stats
+
+    c = CONFIGS["llama8b"]
+    N, D, V = c["N"], c["D"], c["V"]
+    v0, vl = F.shard_range(V, 8, 2)
+    inp = make_config("llama8b", device="cuda")
+    Wsh = inp.weight[v0:v0 + vl].contiguous()
+    comm = F.Comm.single()
+    try:
+        out = F.forward_backward(inp.hidden, Wsh, inp.labels, comm=comm, vocab_start=v0, vocab_total=V,
+                                 with_token_loss=True)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    H = inp.hidden.float().cpu().numpy()
+    Wn = Wsh.float().cpu().numpy()
+    y = inp.labels.cpu().numpy()
+    lse_gpu = out["lse"].cpu().double().numpy()
+    rows = np.random.default_rng(5).choice(N, 256, replace=False)
+    st = shard_stats(H[rows], Wn, y[rows], v0, V)
+    lse_sh = st["m"] + np.log(st["s"])
+    assert np.abs(lse_gpu[rows] - lse_sh).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
+    tok = out["token_loss"].cpu().double().numpy()[rows]
+    assert np.abs(tok - (lse_sh - st["z_target"])).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
+    # the rank's dW rows, with the GPU's (shard-local) lse as the oracle's lse input
+    nv = int((y != IGNORE).sum())
+    dW = np.zeros((vl, D))
+    for a in range(0, N, 2048):
+        dW += shard_backward(H[a:a + 2048], Wn, y[a:a + 2048], v0, lse_gpu[a:a + 2048], 1.0 / nv)["dW_shard"]
+    assert fro_rel(out["dweight"].cpu().double().numpy(), dW) <= GRAD_TOL
+
+
 @pytest.mark.parametrize("path", ["split", "fused"])
 def test_cuda_graph_capture_replays_bitwise(cuda_lib, path):
     """Every launch is stream-ordered with no host sync or allocation, so a
