@@ -9,6 +9,10 @@
 namespace lce {
 
 constexpr float kLog2e = 1.4426950408889634f;
+// scaled-q mode: largest log-ratio exp(z - ref) / exp(lse - ref) kept in the bf16
+// chunk (e^64 ~ 6e27: the dH accumulator over V ~ 1e5 columns stays far below
+// the fp32 range); rows beyond it fall back to the tile-max form
+constexpr float kScaledQMax = 64.f;
 constexpr uint32_t kStatusBadLabel = 1u;
 
 // Device-side header at the start of the workspace.
@@ -55,6 +59,11 @@ struct EpiLse : EpiBase {
     int32_t use_zmap;     // 1: store the fp32 chunk through `zmap` (TMA, 32x32 fp32 boxes, 128B swizzle)
     int32_t store_q;      // 1 (fused CE): store q = exp(z - m_tile) in bf16 through `zmap` (64x32 boxes)
     alignas(64) CUtensorMap zmap;
+    // scaled-q mode (R25): q = exp(z - q_ref[row]) with a per-row reference
+    // instead of the tile max; rows whose tile max exceeds it by more than
+    // kScaledQMax raise *q_flag (the chunk is then redone in the tile-max form)
+    const float* q_ref;
+    int32_t* q_flag;
   };
   static __device__ __forceinline__ void finish(const Params& p) {
     if ((p.use_zmap || p.store_q) && (threadIdx.x & 31) == 0) tma_store_wait_all();
@@ -78,7 +87,7 @@ struct EpiLse : EpiBase {
   // kFull: every column of the tile is < n_cols (no per-element bound checks;
   // same arithmetic and summation order as the checked path)
   template <bool kStoreQ, bool kFull>
-  static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, TileInfo& t, float ml) {
+  static __device__ __forceinline__ float sum_exp(const Params& p, uint32_t taddr, TileInfo& t, float ml, float qf) {
     float s = 0.f;
 #pragma unroll 1
     for (int c2 = 0; c2 < BN / 64; ++c2) {
@@ -95,7 +104,7 @@ struct EpiLse : EpiBase {
           const float e1 = (kFull || cb + j + 1 < p.n_cols) ? ex2_approx(fmaf(x[j + 1], kLog2e, -ml)) : 0.f;
           a0 += e0;
           a1 += e1;
-          if (kStoreQ) w[h * 16 + j / 2] = pack_bf16x2(e0, e1);
+          if (kStoreQ) w[h * 16 + j / 2] = pack_bf16x2(e0 * qf, e1 * qf);  // qf = 1: exact
         }
       }
       s += a0 + a1;
@@ -146,8 +155,15 @@ struct EpiLse : EpiBase {
     }
     const float ml = (m == -INFINITY) ? 0.f : m * kLog2e;
     const bool full = t.n0 + BN <= p.n_cols;
-    const float s = p.store_q ? (full ? sum_exp<true, true>(p, taddr, t, ml) : sum_exp<true, false>(p, taddr, t, ml))
-                              : (full ? sum_exp<false, true>(p, taddr, t, ml) : sum_exp<false, false>(p, taddr, t, ml));
+    // scaled-q mode: the stored q is e * exp(m - ref) = exp(z - ref)
+    float qf = 1.f;
+    if (p.store_q && p.q_ref) {
+      const float dm = m - p.q_ref[p.row_off + r];
+      if (valid && dm > kScaledQMax) *p.q_flag = 1;
+      qf = ex2_approx(fminf(dm, kScaledQMax) * kLog2e);
+    }
+    const float s = p.store_q ? (full ? sum_exp<true, true>(p, taddr, t, ml, qf) : sum_exp<true, false>(p, taddr, t, ml, qf))
+                              : (full ? sum_exp<false, true>(p, taddr, t, ml, qf) : sum_exp<false, false>(p, taddr, t, ml, qf));
     if (valid) {
       p.part_m[t.n_blk * p.ld + r] = m;
       p.part_s[t.n_blk * p.ld + r] = s;
@@ -254,6 +270,7 @@ struct EpiDH : EpiBase {
                            //    TMA reduce-adds (the L2 adds; no read by the SM); unscaled, a
                            //    finalize pass applies c, rounds and scatters
     alignas(64) CUtensorMap map;  // acc_buf [rows, ld] fp32, 32 x 32 boxes, 128B swizzle
+    const float* row_coef;  // scaled-q mode: per chunk-row factor s_i beta_i of the direct path (null: none)
   };
   // pull the running fp32 sum of this tile's row into L2 while the MMA runs
   static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
@@ -309,7 +326,7 @@ struct EpiDH : EpiBase {
       }
       return;
     }
-    const float cs = (p.last_direct && p.use_c) ? p.hdr->c : 1.f;
+    const float cs = ((p.last_direct && p.use_c) ? p.hdr->c : 1.f) * ((p.row_coef && valid) ? p.row_coef[r] : 1.f);
     float* accrow = p.acc_buf + static_cast<int64_t>(p.row_off + r) * p.ld;
     uint16_t* orow = nullptr;
     if (valid && p.last_direct) orow = p.dhidden + static_cast<int64_t>(p.idx[p.row_off + r]) * p.ld;
@@ -818,7 +835,9 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
                                                            const float* __restrict__ zt,
                                                            const int32_t* __restrict__ idx, const Header* hdr,
                                                            float* __restrict__ lse_out, float* __restrict__ tok_out,
-                                                           float* __restrict__ lse_c, float* __restrict__ ltok) {
+                                                           float* __restrict__ lse_c, float* __restrict__ ltok,
+                                                           const float* __restrict__ q_ref = nullptr,
+                                                           int32_t* __restrict__ q_flag = nullptr) {
   const int m = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5);  // one warp per row
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= M) return;
@@ -833,6 +852,7 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
   if (tok_out) tok_out[i] = l;
   lse_c[r] = lse;
   if (ltok) ltok[r] = l;
+  if (q_ref && lse - q_ref[r] > kScaledQMax) *q_flag = 1;  // (p_y - 1) / beta would leave the range
 }
 
 // Vocab-parallel S3 of one row chunk (fused path):
@@ -888,7 +908,9 @@ __global__ void __launch_bounds__(256) fixup_q_kernel(uint16_t* __restrict__ Q, 
                                                       const float* __restrict__ lse_c,
                                                       const float* __restrict__ row_scale, const Header* hdr,
                                                       const float* __restrict__ pm, int64_t ld_pm,
-                                                      const float* __restrict__ zt) {
+                                                      const float* __restrict__ zt,
+                                                      const int32_t* __restrict__ gate = nullptr) {
+  if (gate && *gate == 0) return;  // scaled-q mode without fallback: nothing to fix up
   const int m = blockIdx.x;
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= ((M + 63) & ~63)) return;
@@ -1022,7 +1044,8 @@ __global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict_
                                                         int64_t part_stride, int64_t D, int row_off, int cap,
                                                         const int32_t* __restrict__ idx, const Header* hdr,
                                                         uint16_t* __restrict__ dhidden,
-                                                        float* __restrict__ out_f32 = nullptr) {
+                                                        float* __restrict__ out_f32 = nullptr,
+                                                        const float* __restrict__ row_coef = nullptr) {
   const int m = blockIdx.x;
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= M) return;
@@ -1042,6 +1065,7 @@ __global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict_
     return;
   }
   uint2* dst = reinterpret_cast<uint2*>(dhidden + static_cast<int64_t>(idx[row_off + m]) * D);
+  const float k = row_coef ? row_coef[m] : 1.f;
   for (int v = threadIdx.x; v < D / 4; v += blockDim.x) {
     float4 a = reinterpret_cast<const float4*>(part + static_cast<int64_t>(m) * D)[v];
     for (int s = 1; s < ksplit; ++s) {
@@ -1051,7 +1075,105 @@ __global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict_
       a.z += b.z;
       a.w += b.w;
     }
-    dst[v] = make_uint2(pack_bf16x2(a.x, a.y), pack_bf16x2(a.z, a.w));
+    dst[v] = make_uint2(pack_bf16x2(k * a.x, k * a.y), pack_bf16x2(k * a.z, k * a.w));
+  }
+}
+
+// ============================================================ fused path, scaled-q mode (R25)
+// The per-row reference of the stored probabilities: ref_i = h_i . w_{y_i} in
+// fp32 (the target logit up to summation order; any value within kScaledQMax
+// of the row's logits would do).  One warp per compact row; rows >= N_v get 0.
+__global__ void __launch_bounds__(256) target_dot_kernel(const uint16_t* __restrict__ hc,
+                                                         const uint16_t* __restrict__ W, int64_t D,
+                                                         const int32_t* __restrict__ yc, int32_t label_off,
+                                                         int32_t n_cols, const Header* hdr, int rows,
+                                                         float* __restrict__ q_ref) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int col = r < hdr->n_valid ? yc[r] - label_off : -1;
+  if (col < 0 || col >= n_cols) {
+    if (lane == 0) q_ref[r] = 0.f;
+    return;
+  }
+  const uint4* a = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(r) * D);
+  const uint4* b = reinterpret_cast<const uint4*>(W + static_cast<int64_t>(col) * D);
+  float acc = 0.f;
+  for (int v = lane; v < D / 8; v += 32) {
+    const uint4 x = a[v], w = b[v];
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[j]));
+      const float2 wf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ws[j]));
+      acc = fmaf(xf.x, wf.x, acc);
+      acc = fmaf(xf.y, wf.y, acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) q_ref[r] = acc;
+}
+
+// Scaled-q mode, after the chunk's lse: per chunk row i (one CTA), with
+// s_i = c (or c g_i) and beta_i = exp(ref_i - lse_i):
+//   coef_i = s_i beta_i                 (dH rows: coef_i (q W)_i)
+//   Hs_i   = bf16(s_i beta_i h_i)        (dW = q^T Hs)
+//   q[i, y_i] = bf16((p_y - 1) / beta_i), p_y = exp(z_y - lse_i) from the fp32
+//   target logit, so G = s beta q holds at the target column too (R25).
+// If the chunk's flag is set (some row out of range) the chunk falls back to
+// the tile-max form: coef = 1, Hs = h, and the redo forward + fix-up produce G.
+// Rows in [M, Nc) get zero coefficients and zero Hs rows.  Block 0 also sets
+// the row extent of the conditional redo GEMM (N_v if flagged, else 0).
+__global__ void __launch_bounds__(256) scaled_prep_kernel(uint16_t* __restrict__ Q, int64_t ldq, int row_off,
+                                                          int cap, const uint16_t* __restrict__ hc, int64_t D,
+                                                          const int32_t* __restrict__ yc, int32_t label_off,
+                                                          int32_t n_cols, const float* __restrict__ lse_c,
+                                                          const float* __restrict__ zt,
+                                                          const float* __restrict__ q_ref,
+                                                          const float* __restrict__ row_scale, const Header* hdr,
+                                                          const int32_t* __restrict__ q_flag,
+                                                          int32_t* __restrict__ redo_rows, float* __restrict__ coef,
+                                                          uint16_t* __restrict__ Hs) {
+  const int m = blockIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  const bool fallback = *q_flag != 0;
+  if (m == 0 && threadIdx.x == 0) *redo_rows = fallback ? hdr->n_valid : 0;
+  uint4* hs = reinterpret_cast<uint4*>(Hs + static_cast<int64_t>(m) * D);
+  if (m >= M) {
+    if (threadIdx.x == 0) coef[m] = 0.f;
+    for (int v = threadIdx.x; v < D / 8; v += blockDim.x) hs[v] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const int r = row_off + m;
+  const uint4* h = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(r) * D);
+  if (fallback) {
+    if (threadIdx.x == 0) coef[m] = 1.f;
+    for (int v = threadIdx.x; v < D / 8; v += blockDim.x) hs[v] = h[v];
+    return;
+  }
+  const float lse = lse_c[r];
+  const float beta = ex2_approx((q_ref[r] - lse) * kLog2e);
+  const float k = hdr->c * (row_scale ? row_scale[r] : 1.f) * beta;
+  if (threadIdx.x == 0) {
+    coef[m] = k;
+    const int col = yc[r] - label_off;
+    if (col >= 0 && col < n_cols) {
+      const float py = ex2_approx((zt[r] - lse) * kLog2e);
+      __nv_bfloat16 g = __float2bfloat16_rn((py - 1.f) / beta);
+      Q[static_cast<int64_t>(m) * ldq + col] = *reinterpret_cast<uint16_t*>(&g);
+    }
+  }
+  for (int v = threadIdx.x; v < D / 8; v += blockDim.x) {
+    const uint4 x = h[v];
+    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[j]));
+      o[j] = pack_bf16x2(k * f.x, k * f.y);
+    }
+    hs[v] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 

@@ -126,6 +126,7 @@ struct FusedPlan {
   int wide_dh, wide_dw;            // 512 x 256 tiles for the chunk's dH / dW GEMMs
   size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, slab;
   size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
+  size_t qref, coef, hs, qflag;    // scaled-q mode (R25): per-row reference, dH row factors, scaled H chunk, flags
   size_t total;
 };
 
@@ -208,6 +209,12 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   q.vmglob = take(static_cast<size_t>(q.Nc * 4));
   q.vsz = take(static_cast<size_t>(q.Nc * 8));
   q.vdh = take(static_cast<size_t>(q.Nc * q.D * 4));  // fp32 dH chunk (vocab-parallel only)
+  if (!kd) {  // the KD path keeps fp32 logits and never uses the scaled-q form
+    q.qref = take(static_cast<size_t>(q.n_chunks * q.Nc * 4));
+    q.coef = take(static_cast<size_t>(q.Nc * 4));
+    q.hs = take(static_cast<size_t>(q.Nc * q.D * 2));
+    q.qflag = take(2 * sizeof(int32_t));
+  }
   q.total = off;
   *fp = q;
   return true;
@@ -948,19 +955,20 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
 lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStream_t s, Header* hdr,
                          const CUtensorMap& t_g_k, const CUtensorMap& t_w_mn, const CUtensorMap& t_g_mn,
                          const CUtensorMap& t_h_mn, int32_t r0, float* slab, float* vdh, const int32_t* idx,
-                         uint16_t* dhidden, float* dweight, bool accumulate) {
+                         uint16_t* dhidden, float* dweight, bool accumulate, const float* row_coef = nullptr) {
   const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
   const int split = fp.split;
   {
     GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
     float* part = split > 1 ? slab : (comm ? vdh : nullptr);
     EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
+    ep.row_coef = row_coef;
     LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s, fp.wide_dh)));
   }
   if (split > 1) {
     LaunchScope sc(LCE_K_FINAL, s);
     reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(slab, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                 dhidden, comm ? vdh : nullptr);
+                                                                 dhidden, comm ? vdh : nullptr, row_coef);
     LCE_TRY(last_error());
   }
   if (comm) {
@@ -1087,17 +1095,41 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   LCE_TRY(map_mnmajor(&t_w_mn, weight, fp.Vl, fp.D, fp.D));
   LCE_TRY(map_kmajor(&t_g_k, G, fp.Nc, fp.ldv, fp.ldv, BM));
   LCE_TRY(map_mnmajor(&t_g_mn, G, fp.Nc, fp.ldv, fp.ldv));
+  // Scaled-q form (R25): q relative to a per-row reference
+  // (the target logit), so the row factors of G move into the dH epilogue and
+  // the dW GEMM's B operand and the HBM-bound fix-up pass is skipped; chunks
+  // with out-of-range rows redo their forward in the tile-max form on the GPU
+  // (no host sync).  One GPU and token parallelism; LCE_FUSED_SCALED=0 selects
+  // the fix-up form.
+  const bool scaled = !comm && !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
+  float* qref = reinterpret_cast<float*>(ws + fp.qref);
+  float* coef = reinterpret_cast<float*>(ws + fp.coef);
+  uint16_t* hs = reinterpret_cast<uint16_t*>(ws + fp.hs);
+  int32_t* qflag = reinterpret_cast<int32_t*>(ws + fp.qflag);
+  int32_t* redo_rows = qflag + 1;
+  CUtensorMap t_hs_mn;
+  if (scaled) {
+    LCE_TRY(map_mnmajor(&t_hs_mn, hs, fp.Nc, fp.D, fp.D));
+    LaunchScope sc(LCE_K_GATHER, s);
+    const int rows = static_cast<int>(fp.n_chunks * fp.Nc);
+    target_dot_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
+        hc, weight, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, hdr, rows, qref);
+    LCE_TRY(last_error());
+  }
   for (int64_t q = 0; q < fp.n_chunks; ++q) {
     const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
     const uint16_t* hq = hc + static_cast<int64_t>(r0) * fp.D;
     CUtensorMap t_h_k, t_h_mn;
     LCE_TRY(map_kmajor(&t_h_k, hq, fp.Nc, fp.D, fp.D, BM));
     LCE_TRY(map_mnmajor(&t_h_mn, hq, fp.Nc, fp.D, fp.D));
-    // S1+S2 (+ keep q = exp(z - m_tile) of the chunk in bf16): z = H_q W^T, LSE partials
+    if (scaled) LCE_CUDA(cudaMemsetAsync(qflag, 0, sizeof(int32_t), s));
+    // S1+S2 (+ keep q of the chunk in bf16): z = H_q W^T, LSE partials
     {
       GemmDims d{&hdr->n_valid, 0, nullptr, D, Vl, r0, Nc, 0, 0};
       EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, nullptr, fp.ldv};
       ep.store_q = 1;
+      ep.q_ref = scaled ? qref : nullptr;
+      ep.q_flag = scaled ? qflag : nullptr;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
@@ -1105,7 +1137,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
     if (!comm) {  // S3 for the chunk rows
       LaunchScope sc(LCE_K_COMBINE, s);
       combine_rows_kernel<<<cb, 256, 0, s>>>(pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse,
-                                            token_loss, lsec, ltok);
+                                            token_loss, lsec, ltok, scaled ? qref : nullptr,
+                                            scaled ? qflag : nullptr);
       LCE_TRY(last_error());
     } else {  // vocab-parallel S3: MAX of m, rescale, SUM of (s, z_t) over the chunk rows
       const int nt = static_cast<int>(fp.n_tiles);
@@ -1130,15 +1163,33 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
         LCE_TRY(last_error());
       }
     }
+    if (scaled) {  // row factors, scaled H chunk, target column; fallback extent
+      {
+        LaunchScope sc(LCE_K_BWD_G, s);
+        scaled_prep_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(
+            G, fp.ldv, r0, Nc, hc, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, lsec, zt, qref,
+            row_grad ? gsc : nullptr, hdr, qflag, redo_rows, coef, hs);
+        LCE_TRY(last_error());
+      }
+      // fallback (device-decided, empty unless a row was out of range): the
+      // forward again with tile-max q, then the fix-up below
+      GemmDims d{redo_rows, 0, nullptr, D, Vl, r0, Nc, 0, 0};
+      EpiLse::Params ep{yc, static_cast<int32_t>(p->vocab_start), Vl, pm, ps, fp.Nc, zt, r0, nullptr, fp.ldv};
+      ep.store_q = 1;
+      LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
+      LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_BWD_G, t_h_k, t_w_k, d, ep, dev.sms, s)));
+    }
     {  // S4 without recompute: G = s_i (softmax - onehot) from the kept q, in place
+      // (scaled form: only on the fallback)
       LaunchScope sc(LCE_K_BWD_G, s);
       fixup_q_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(G, fp.ldv, Vl, r0, Nc, yc,
                                                                   static_cast<int32_t>(p->vocab_start), lsec,
-                                                                  row_grad ? gsc : nullptr, hdr, pm, fp.Nc, zt);
+                                                                  row_grad ? gsc : nullptr, hdr, pm, fp.Nc, zt,
+                                                                  scaled ? redo_rows : nullptr);
       LCE_TRY(last_error());
     }
-    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, t_h_mn, r0, slab, vdh, idx, dhidden,
-                        dweight, q > 0 || accumulate_dweight));
+    LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, scaled ? t_hs_mn : t_h_mn, r0, slab, vdh,
+                        idx, dhidden, dweight, q > 0 || accumulate_dweight, scaled ? coef : nullptr));
   }
   {
     LaunchScope sc(LCE_K_COMBINE, s);

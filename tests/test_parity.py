@@ -372,6 +372,39 @@ def test_token_parallel_decomposition(cuda_lib, path):
     assert np.abs(np.concatenate(tok) - o["tok"]).max() <= LSE_TOL * max(1.0, np.abs(o["lse"]).max())
 
 
+@pytest.mark.parametrize("reduction", ["mean", "none"])
+def test_fused_scaled_q_fallback_rows(cuda_lib, reduction):
+    """R25: the fused path keeps q relative to each row's target logit; a chunk
+    with a row whose logits exceed it by more than e^64 (a target logit ~100
+    below the row's lse) redoes its forward in the tile-max form on the GPU.
+    Both chunks -- one with such rows, one without -- match the oracle, and so
+    do the unscaled fix-up form and a confident (p_target ~ 1) batch."""
+    N, D, V = 700, 128, 3000
+    inp = small(N, D, V, seed=31, ignore_frac=0.1)
+    lab = inp.labels.cpu().numpy()
+    # rows 5..20 (first chunk): push the target logit ~100 below the others
+    y = inp.labels.long().clamp(min=0)
+    Wy = inp.weight[y].float()
+    bump = -100.0 * Wy / (Wy * Wy).sum(dim=1, keepdim=True)
+    rows = torch.zeros(N, dtype=torch.bool, device="cuda")
+    rows[5:21] = True
+    rows &= inp.labels != IGNORE
+    h = torch.where(rows[:, None], inp.hidden.float() + bump, inp.hidden.float()).to(torch.bfloat16)
+    spiky = LceInputs(hidden=h.contiguous(), weight=inp.weight, labels=inp.labels)
+    g = None if reduction == "mean" else np.linspace(-1.0, 2.0, N)
+    budget = 256 * 2 * 3072  # 512-row chunks: rows 0..511 flagged, the rest not
+    for case in (spiky, small(N, D, V, seed=32, regime="confident")):
+        o = oracle_run(case, reduction, grad=1.0 if g is None else g)
+        assert o["loss"] > 0
+        assert_parity(fused_run(case, reduction, grad=g, budget=budget), o, case.labels.cpu().numpy())
+    os.environ["LCE_FUSED_SCALED"] = "0"
+    try:
+        o = oracle_run(spiky, reduction, grad=1.0 if g is None else g)
+        assert_parity(fused_run(spiky, reduction, grad=g, budget=budget), o, lab)
+    finally:
+        del os.environ["LCE_FUSED_SCALED"]
+
+
 def test_autograd_function(cuda_lib):
     import paper_2605_21442_b200 as F
 
