@@ -311,6 +311,7 @@ struct EpiDH : EpiBase {
     }
     if (p.part) {  // split-K partial: plain fp32 store, no read-modify-write
       float* prow = p.part + t.split * p.part_stride + static_cast<int64_t>(r) * p.ld;
+      const float rc = (p.row_coef && valid) ? p.row_coef[r] : 1.f;  // linear: each slab scaled
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float x[32];
@@ -321,7 +322,8 @@ struct EpiDH : EpiBase {
         for (int v = 0; v < 8; ++v) {
           const int col = cb + 4 * v;
           if (col >= t.N) break;
-          *reinterpret_cast<float4*>(prow + col) = make_float4(x[4 * v], x[4 * v + 1], x[4 * v + 2], x[4 * v + 3]);
+          *reinterpret_cast<float4*>(prow + col) =
+              make_float4(rc * x[4 * v], rc * x[4 * v + 1], rc * x[4 * v + 2], rc * x[4 * v + 3]);
         }
       }
       return;
@@ -867,7 +869,9 @@ __global__ void __launch_bounds__(256) combine_chunk_vp_kernel(int mode, const f
                                                                float* __restrict__ sz, const int32_t* __restrict__ idx,
                                                                const Header* hdr, float* __restrict__ lse_out,
                                                                float* __restrict__ tok_out, float* __restrict__ lse_c,
-                                                               float* __restrict__ ltok) {
+                                                               float* __restrict__ ltok,
+                                                               const float* __restrict__ q_ref = nullptr,
+                                                               int32_t* __restrict__ q_flag = nullptr) {
   // one warp per chunk row (8 rows per CTA); lane 0 owns the row
   const int m = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5);
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
@@ -895,6 +899,7 @@ __global__ void __launch_bounds__(256) combine_chunk_vp_kernel(int mode, const f
   if (tok_out) tok_out[i] = l;
   lse_c[r] = lse;
   if (ltok) ltok[r] = l;
+  if (q_ref && lse - q_ref[r] > kScaledQMax) *q_flag = 1;
 }
 
 // S4 of the fused CE path, in place: q = exp(z - m_t) (bf16, stored by the

@@ -968,7 +968,7 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
   if (split > 1) {
     LaunchScope sc(LCE_K_FINAL, s);
     reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(slab, split, fp.Nc * fp.D, fp.D, r0, Nc, idx, hdr,
-                                                                 dhidden, comm ? vdh : nullptr, row_coef);
+                                                                 dhidden, comm ? vdh : nullptr);
     LCE_TRY(last_error());
   }
   if (comm) {
@@ -1099,9 +1099,9 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   // (the target logit), so the row factors of G move into the dH epilogue and
   // the dW GEMM's B operand and the HBM-bound fix-up pass is skipped; chunks
   // with out-of-range rows redo their forward in the tile-max form on the GPU
-  // (no host sync).  One GPU and token parallelism; LCE_FUSED_SCALED=0 selects
-  // the fix-up form.
-  const bool scaled = !comm && !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
+  // (no host sync; under vocab parallelism each rank decides for its own
+  // partials).  LCE_FUSED_SCALED=0 selects the fix-up form.
+  const bool scaled = !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
   float* qref = reinterpret_cast<float*>(ws + fp.qref);
   float* coef = reinterpret_cast<float*>(ws + fp.coef);
   uint16_t* hs = reinterpret_cast<uint16_t*>(ws + fp.hs);
@@ -1116,6 +1116,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
         hc, weight, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, hdr, rows, qref);
     LCE_TRY(last_error());
   }
+  // vocab-parallel: the target row of W lives on one rank (the others add 0)
+  if (scaled && comm) LCE_TRY(allreduce(comm, qref, static_cast<size_t>(fp.n_chunks * fp.Nc), ncclSum, s));
   for (int64_t q = 0; q < fp.n_chunks; ++q) {
     const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
     const uint16_t* hq = hc + static_cast<int64_t>(r0) * fp.D;
@@ -1159,7 +1161,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       {
         LaunchScope sc(LCE_K_COMBINE, s);
         combine_chunk_vp_kernel<<<cb, 256, 0, s>>>(3, pm, ps, nt, fp.Nc, r0, Nc, zt, vmloc, vmglob, vsz, idx, hdr,
-                                                   lse, token_loss, lsec, ltok);
+                                                   lse, token_loss, lsec, ltok, scaled ? qref : nullptr,
+                                                   scaled ? qflag : nullptr);
         LCE_TRY(last_error());
       }
     }
