@@ -20,11 +20,11 @@ from collections import OrderedDict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CLASS = OrderedDict([
+    ("scaled_prep_kernel", "bwd_g"), ("target_dot_kernel", "gather"),
     ("EpiLse", "fwd_gemm"), ("EpiG", "bwd_g"), ("EpiDH", "bwd_dh"), ("EpiDW", "bwd_dw"),
     ("prep_kernel", "prep"), ("gather_kernel", "gather"), ("combine_kernel", "combine"),
     ("combine_rows_kernel", "combine"), ("loss_reduce_kernel", "combine"), ("fixup_g_kernel", "bwd_g"), ("fixup_q_kernel", "bwd_g"),
     ("finalize_dh_kernel", "finalize"), ("reduce_dh_kernel", "finalize"), ("EpiAdamW", "bwd_dw"),
-    ("scaled_prep_kernel", "bwd_g"), ("target_dot_kernel", "gather"),
 ])
 
 
