@@ -277,6 +277,31 @@ def test_deterministic_rerun(cuda_lib):
     assert a["loss"] == b["loss"]
 
 
+@pytest.mark.parametrize("gemm", ["default", "pair"])
+def test_fused_deterministic_and_mask_first(cuda_lib, monkeypatch, gemm):
+    """H8 and P3 for the fused path at a shape that takes its wide dH / dW tiles
+    (8,192-row chunks), split-K dH and the TMA reduce-add of the second chunk's
+    dW: two runs are bitwise identical, and NaN / Inf in ignored rows of H leave
+    every output bitwise unchanged (their dH rows exactly 0)."""
+    if gemm == "default":
+        monkeypatch.delenv("LCE_GEMM", raising=False)
+    else:
+        monkeypatch.setenv("LCE_GEMM", gemm)
+    inp = small(16384, 256, 5000, seed=33, ignore_frac=0.2)
+    a, b = fused_run(inp), fused_run(inp)
+    for k in ("lse", "tok", "dH", "dW"):
+        np.testing.assert_array_equal(a[k], b[k])
+    assert a["loss"] == b["loss"]
+    ign = inp.labels == IGNORE
+    h = inp.hidden.clone()
+    h[ign] = float("nan")
+    h[torch.nonzero(ign)[0, 0]] = float("inf")
+    c = fused_run(LceInputs(hidden=h, weight=inp.weight, labels=inp.labels))
+    for k in ("lse", "tok", "dH", "dW"):
+        np.testing.assert_array_equal(a[k], c[k])
+    assert a["loss"] == c["loss"] and np.all(c["dH"][ign.cpu().numpy()] == 0)
+
+
 def test_single_rank_communicator_path(cuda_lib):
     """The vocab-parallel exchange (MAX / SUM all-reduce + finalize) on a
     one-rank NCCL communicator matches the oracle."""
