@@ -16,6 +16,10 @@
 //               one TMEM lane) while the MMA warp fills the other buffer.
 // Pipelines: smem full/empty mbarriers (TMA <-> MMA, kStages deep) and TMEM
 // full/empty mbarriers (MMA <-> epilogue, 2 deep).
+// Three variants share this structure: gemm_kernel (one CTA, 128x256 tiles),
+// gemm_pair_kernel (CTA pair, cta_group::2, 256x256 tiles, the default) and
+// gemm_wide_kernel (CTA pair, 512x256 tiles, one accumulator per CTA half).
+// Under the profiler CTA 0 records its clock64 / %globaltimer span (probe).
 #pragma once
 
 #include "sm100.cuh"

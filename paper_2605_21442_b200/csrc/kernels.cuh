@@ -39,10 +39,11 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // tile column n_blk; the logits never leave the SM (the dense [B,S,V]
 // tensor is never materialised).  Every path uses the same passes and the
 // same summation order, so lse is bitwise identical across them.
-//   fused CE path (store_q): pass 2 also stores e rounded to bf16 (q, in
-//     [0, 1]; 2 bytes per logit) so the G fix-up can rescale it by
-//     exp(m - lse) (R24).  Logits are never rounded (R8): only the
-//     probabilities relative to the tile max are.
+//   fused CE path (store_q): pass 2 also stores e rounded to bf16 (2 bytes
+//     per logit) -- relative to a per-row reference, q = e * exp(m - ref) =
+//     exp(z - ref) (scaled-q form, q_ref set, R25), or relative to
+//     the tile max (q = e in [0, 1], R24, for the G fix-up).  Logits are never
+//     rounded (R8): only probabilities relative to a reference are.
 //   KD path (use_zmap / z): pass 1 stores the fp32 logits.
 struct EpiLse : EpiBase {
   struct Params {
