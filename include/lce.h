@@ -41,7 +41,9 @@
 extern "C" {
 #endif
 
-#define LCE_ABI_VERSION 1
+/* 2: lce_comm_init_mode / lce_comm_mode (token-parallel communicators) and
+ *    lce_profile_read_clocks; n_valid reports the global N_v in token mode. */
+#define LCE_ABI_VERSION 2
 
 typedef enum {
   LCE_OK = 0,

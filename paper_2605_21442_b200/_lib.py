@@ -57,12 +57,19 @@ class Problem(ctypes.Structure):
     ]
 
 
+ABI_VERSION = 2  # include/lce.h LCE_ABI_VERSION
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python paper_2605_21442_b200/build.py` "
             "(there is deliberately no fallback implementation)")
     lib = ctypes.CDLL(LIB_PATH)
+    lib.lce_abi_version.restype = ctypes.c_int
+    if lib.lce_abi_version() != ABI_VERSION:  # a stale build of the library
+        raise ImportError(f"{LIB_PATH} has ABI {lib.lce_abi_version()}, this binding needs {ABI_VERSION}: "
+                          "rebuild it with `python paper_2605_21442_b200/build.py`")
     P = ctypes.POINTER
     vp, i32p, f32p = ctypes.c_void_p, P(ctypes.c_int32), P(ctypes.c_float)
     lib.lce_workspace_bytes.argtypes = [P(Problem)]

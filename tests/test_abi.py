@@ -38,7 +38,7 @@ def test_exports_every_header_symbol(L):
 
 
 def test_version_and_status_strings(L):
-    assert L.lib.lce_abi_version() == 1
+    assert L.lib.lce_abi_version() == L.ABI_VERSION == 2
     for code in range(11):
         s = L.lib.lce_status_string(code)
         assert s and s != b"unknown status"
