@@ -430,6 +430,44 @@ def test_fused_scaled_q_fallback_rows(cuda_lib, reduction):
         del os.environ["LCE_FUSED_SCALED"]
 
 
+def test_fused_scaled_q_vocab_shard_fallback(cuda_lib):
+    """R25 under a one-rank vocab-parallel communicator over a shard: the
+    per-row references are exchanged (rows whose label lies outside the shard
+    get 0), rows with a target ~100 nats below the shard's logits flag their
+    chunk, and the result is still the oracle's shard statistics / gradients."""
+    import paper_2605_21442_b200 as F
+    from oracle import shard_backward, shard_stats
+
+    N, D, V, v0, vl = 700, 128, 3000, 1000, 1500
+    inp = small(N, D, V, seed=34, ignore_frac=0.1)
+    y = inp.labels.long().clamp(min=0)
+    Wy = inp.weight[y].float()
+    own = (inp.labels >= v0) & (inp.labels < v0 + vl)
+    rows = torch.zeros(N, dtype=torch.bool, device="cuda")
+    rows[:40] = True
+    rows &= own
+    h = torch.where(rows[:, None], inp.hidden.float() - 100.0 * Wy / (Wy * Wy).sum(1, keepdim=True),
+                    inp.hidden.float()).to(torch.bfloat16).contiguous()
+    Wsh = inp.weight[v0:v0 + vl].contiguous()
+    comm = F.Comm.single()
+    try:
+        out = F.forward_backward(h, Wsh, inp.labels, comm=comm, vocab_start=v0, vocab_total=V, with_token_loss=True,
+                                 chunk_budget_bytes=256 * 2 * 1536)
+        torch.cuda.synchronize()
+    finally:
+        comm.close()
+    H = h.float().cpu().numpy()
+    Wn = Wsh.float().cpu().numpy()
+    lab = inp.labels.cpu().numpy()
+    st = shard_stats(H, Wn, lab, v0, V)
+    valid = st["valid"]
+    lse_sh = np.where(valid, st["m"] + np.log(np.where(valid, st["s"], 1.0)), 0.0)
+    assert np.abs(out["lse"].cpu().double().numpy() - lse_sh).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
+    sb = shard_backward(H, Wn, lab, v0, lse_sh, 1.0 / int(valid.sum()))
+    assert fro_rel(out["dhidden"].float().cpu().double().numpy(), sb["dH_partial"]) <= GRAD_TOL
+    assert fro_rel(out["dweight"].cpu().double().numpy(), sb["dW_shard"]) <= GRAD_TOL
+
+
 def test_autograd_function(cuda_lib):
     import paper_2605_21442_b200 as F
 
