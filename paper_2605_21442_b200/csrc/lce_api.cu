@@ -119,6 +119,7 @@ constexpr int kPlanSms = 148;  // B200: the split-K choice is made at plan time 
 // least this many: shorter k-ranges leave the epilogue of the wide kernel's
 // single accumulator exposed (measured: DESIGN.md section 5)
 constexpr int64_t kWideMinRows = 8192;
+constexpr int64_t kWideMinDhK = 12288;
 
 struct FusedPlan {
   int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
@@ -182,10 +183,16 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   q.Nc = round_up(ceil_div(q.cap, q.n_chunks), kPairBM);  // balanced chunks
   // wide tiles pay off once a dW work item's K (= the chunk's rows) is long
   // enough to hide the epilogue of the unbuffered accumulator
-  q.wide_dh = use_pair() && use_wide(LCE_K_BWD_DH, q.Nc >= kWideMinRows ? 1 : 0);
+  // ... and, for dH (K = V_l, split-K), when each work item still reduces over
+  // >= kWideMinDhK vocab columns (vocab-parallel shards are short; per-rank 8B
+  // step on one GPU, scripts/bench_shard.py: at P = 8 (8,016 columns per item)
+  // pair tiles were 5% faster per step, at P = 4 (16,032) and P = 2 (32,064)
+  // wide tiles 1-4% faster)
+  const int max_split = kd ? static_cast<int>(q.ldv / q.D) : 8;
+  const int split_wide = dh_split(q.Nc, q.D, max_split, kPlanSms, kWideBM);
+  q.wide_dh = use_pair() && use_wide(LCE_K_BWD_DH, (q.Nc >= kWideMinRows && q.Vl / split_wide >= kWideMinDhK) ? 1 : 0);
   q.wide_dw = use_pair() && use_wide(LCE_K_BWD_DW, q.Nc >= kWideMinRows ? 1 : 0);
-  q.split = dh_split(q.Nc, q.D, kd ? static_cast<int>(q.ldv / q.D) : 8, kPlanSms,
-                     !use_pair() ? BM : (q.wide_dh ? kWideBM : kPairBM));
+  q.split = dh_split(q.Nc, q.D, max_split, kPlanSms, !use_pair() ? BM : (q.wide_dh ? kWideBM : kPairBM));
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
