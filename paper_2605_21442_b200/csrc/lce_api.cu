@@ -61,14 +61,15 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
   q.Vl = Vl;
   q.cap = round_up(N > 0 ? N : 1, kPairBM);  // whole 256-row pair tiles (G rows are written per tile)
   q.n_tiles = ceil_div(Vl, BN);
-  // Default G chunk: 16384 vocab columns, as bytes clamped to [512 MiB, 4 GiB],
-  // and never fewer than 4096 columns.  Every chunk re-reads and re-writes
-  // the fp32 dH accumulator (8 N D bytes) against 6 N V_c D flops of GEMMs, so
-  // wide chunks keep that traffic small; for ~1M-token contexts (App. A) the
-  // 4 GiB cap and the 4096-column floor bound the chunk instead.
+  // Default G chunk: 32768 vocab columns, as bytes clamped to [512 MiB, 4 GiB],
+  // and never fewer than 4096 columns.  Every chunk adds into the fp32 dH
+  // accumulator (8 N D bytes through the L2) against 6 N V_c D flops of GEMMs,
+  // and has its own GEMM tails, so wide chunks pay (8B: 32768 columns = 1 GiB
+  // ran 2% faster than 16384 for +0.54 GB of peak HBM); for ~1M-token
+  // contexts (App. A) the 4 GiB cap and the 4096-column floor bound the chunk.
   int64_t budget = p->chunk_budget_bytes;
   if (budget <= 0) {
-    budget = q.cap * 2 * 16384;
+    budget = q.cap * 2 * 32768;
     budget = budget < kDefaultChunkBudget ? kDefaultChunkBudget : (budget > (4ll << 30) ? (4ll << 30) : budget);
     if (budget < q.cap * 2 * 4096) budget = q.cap * 2 * 4096;
   }
