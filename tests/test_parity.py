@@ -428,6 +428,29 @@ def test_fused_scaled_q_fallback_rows(cuda_lib, reduction):
         assert_parity(fused_run(spiky, reduction, grad=g, budget=budget), o, lab)
     finally:
         del os.environ["LCE_FUSED_SCALED"]
+    # the fallback really ran for the spiky batch (and only there): its
+    # tile-max re-forward shows up as GEMM work in the G-formation class
+    import paper_2605_21442_b200 as F
+
+    import ctypes
+
+    def g_gemm_cycles(case):
+        """SM cycles the G-formation class's GEMM launches (the re-forwards) spent."""
+        fused_run(case, reduction, grad=g, budget=budget)
+        F.profile_read()
+        F.profile_enable(True)
+        fused_run(case, reduction, grad=g, budget=budget)
+        k = 9  # LCE_K_COUNT
+        ms, n = (ctypes.c_double * k)(), (ctypes.c_int64 * k)()
+        cyc, ns = (ctypes.c_double * k)(), (ctypes.c_double * k)()
+        assert F.lib.lce_profile_read_clocks(ms, n, cyc, ns) == 0
+        F.profile_enable(False)
+        return cyc[4], n[4]  # LCE_K_BWD_G
+    calm = small(N, D, V, seed=31, ignore_frac=0.1)
+    cyc_spiky, n_spiky = g_gemm_cycles(spiky)
+    cyc_calm, n_calm = g_gemm_cycles(calm)
+    assert n_spiky == n_calm  # the same launches: the redo is empty unless a row flagged its chunk
+    assert cyc_spiky > 3 * cyc_calm, (cyc_spiky, cyc_calm)
 
 
 def test_fused_scaled_q_vocab_shard_fallback(cuda_lib):
