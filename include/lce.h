@@ -42,8 +42,11 @@ extern "C" {
 #endif
 
 /* 2: lce_comm_init_mode / lce_comm_mode (token-parallel communicators) and
- *    lce_profile_read_clocks; n_valid reports the global N_v in token mode. */
-#define LCE_ABI_VERSION 2
+ *    lce_profile_read_clocks; n_valid reports the global N_v in token mode.
+ * 3: dweight_flags (LCE_DW_ACCUMULATE | LCE_DW_BF16) replace accumulate_dweight
+ *    (0 / 1 keep their meaning) and dweight is void*; lce_expect_grad,
+ *    lce_comm_check; LCE_ERR_ARG, LCE_ERR_UPSTREAM. */
+#define LCE_ABI_VERSION 3
 
 typedef enum {
   LCE_OK = 0,
@@ -56,8 +59,21 @@ typedef enum {
   LCE_ERR_DEVICE = 7,      /* current device is not sm_100 (B200)              */
   LCE_ERR_CUDA = 8,        /* a CUDA runtime / driver call failed              */
   LCE_ERR_NCCL = 9,        /* NCCL missing or an NCCL call failed              */
-  LCE_ERR_COMM = 10        /* communicator does not match the problem          */
+  LCE_ERR_COMM = 10,       /* communicator does not match the problem          */
+  LCE_ERR_ARG = 11,        /* unsupported flag combination                     */
+  LCE_ERR_UPSTREAM = 12    /* upstream gradient differs from the one the fused
+                              call assumed (see lce_expect_grad)               */
 } lce_status_t;
+
+/* dweight_flags of the backward entry points (a bit set).
+ *  LCE_DW_ACCUMULATE: dweight += dW instead of dweight = dW (fp32 only;
+ *    gradient accumulation).
+ *  LCE_DW_BF16: dweight is bf16 [V_l, D] (RNE from the fp32 GEMM accumulator,
+ *    written once) instead of fp32.  lce_backward only -- its dW row blocks
+ *    are final when they leave the tensor memory; the fused / KD paths sum dW
+ *    over row chunks in fp32 and return LCE_ERR_ARG for it, as does
+ *    LCE_DW_BF16 | LCE_DW_ACCUMULATE. */
+enum { LCE_DW_ACCUMULATE = 1, LCE_DW_BF16 = 2 };
 
 /* MEAN: L = sum_i loss_i / N_v.  SUM: L = sum_i loss_i.
  * NONE (per-token, the log-prob interface GRPO/DPO need -- P:322, P:463,
@@ -97,8 +113,12 @@ typedef struct {
   int64_t vocab_total;   /* V: labels must lie in [0, V) unless ignored             */
   int32_t ignore_index;  /* rows with this label are dropped before projection      */
   int32_t reduction;     /* lce_reduction_t                                         */
-  int64_t chunk_budget_bytes; /* bytes for one bf16 G chunk in the backward; 0 =
-                                 default (512 MiB).  A performance knob only.       */
+  int64_t chunk_budget_bytes; /* bytes of the bounded chunk buffer; 0 = default:
+                                 lce_backward: 32768 vocab columns of bf16 G
+                                 (2 * ceil256(N) * 32768 bytes) clamped to
+                                 [512 MiB, 4 GiB] and never below 4096 columns;
+                                 lce_forward_backward: 2 GiB of bf16 q/G rows;
+                                 KD: 4 GiB.  A performance knob only.            */
 } lce_problem_t;
 
 /* Bytes of caller-provided device workspace both lce_forward and lce_backward
@@ -137,15 +157,17 @@ lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm,
  *   grad_loss  fp32 in (device) or NULL for 1.0: MEAN / SUM: [1], g = dL_total/dL;
  *              NONE: [N], g_i = dL_total/dloss_i (ignored rows' entries unused)
  *   dhidden    [N, D] bf16 out: dH (RNE from fp32); rows of ignored tokens 0
- *   dweight    [V_l, D] fp32 out: dW for this rank's rows
- *   accumulate_dweight  0: dweight = dW, 1: dweight += dW
+ *   dweight    [V_l, D] fp32 (or bf16 with LCE_DW_BF16) out: dW for this
+ *              rank's rows
+ *   dweight_flags  0: dweight = dW (fp32); LCE_DW_ACCUMULATE: dweight += dW;
+ *              LCE_DW_BF16: bf16 dweight = RNE(dW) (LCE_ERR_ARG with ACCUMULATE)
  * With comm != NULL, dH is summed over ranks (NCCL all-reduce) and is the
  * same on all ranks; dweight is the local shard (concatenate in rank order). */
 lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm,
                           const uint16_t* hidden, const uint16_t* weight,
                           const int32_t* labels, const float* lse,
                           const float* grad_loss, uint16_t* dhidden,
-                          float* dweight, int accumulate_dweight,
+                          void* dweight, int dweight_flags,
                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- optimizer-in-backward for the LM head (Sec. 4.1) -----------
@@ -186,7 +208,9 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
  * bytes, never N x V_l), the rows are reduced to lse, q is turned into G in
  * place and consumed by the dH and dW GEMMs: 6 N_v V D flops instead of 8.
  * The upstream gradient must be known up front (grad_loss as in lce_backward;
- * NULL = 1).  dW is accumulated across row chunks in fp32.  Nc is set by
+ * NULL = 1; lce_expect_grad checks an autograd caller's actual one later).
+ * dW is accumulated across row chunks in fp32 (dweight_flags: 0 or
+ * LCE_DW_ACCUMULATE; LCE_DW_BF16 -> LCE_ERR_ARG).  Nc is set by
  * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB) and is at
  * most half the rows, so the buffer never holds all N x V_l probabilities.
  * With a vocab-parallel comm each row chunk's (max, sum-exp, target
@@ -200,7 +224,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
                                   const int32_t* labels, const float* grad_loss,
                                   float* loss, float* lse, float* token_loss,
                                   int32_t* n_valid, uint16_t* dhidden, float* dweight,
-                                  int accumulate_dweight, void* workspace,
+                                  int dweight_flags, void* workspace,
                                   size_t workspace_bytes, void* stream);
 
 /* ---- linear knowledge distillation (NEXT-4) ----------------
@@ -210,7 +234,8 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm,
  * for rows with labels[i] != ignore_index (label values are only a mask),
  * z_S = H_S W_S^T, z_T = H_T W_T^T, reductions as lce_problem_t.reduction.
  * Student gradients dz_S = s_i (p_S - p_T):  dhidden_s = dz_S W_S (bf16),
- * dweight_s = dz_S^T H_S (fp32, overwrite or accumulate); the teacher gets none.
+ * dweight_s = dz_S^T H_S (fp32; dweight_flags 0 or LCE_DW_ACCUMULATE); the
+ * teacher gets none.
  *   p->hidden_dim = D_S, teacher_dim = D_T (% 8 == 0); hidden_s [N, D_S],
  *   weight_s [V, D_S], hidden_t [N, D_T], weight_t [V, D_T] (bf16);
  *   grad_loss / loss / token_loss / n_valid as lce_forward_backward.
@@ -225,14 +250,27 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm, in
                                      const int32_t* labels, const float* grad_loss,
                                      float* loss, float* token_loss, int32_t* n_valid,
                                      uint16_t* dhidden_s, float* dweight_s,
-                                     int accumulate_dweight, void* workspace,
+                                     int dweight_flags, void* workspace,
                                      size_t workspace_bytes, void* stream);
 
 /* Synchronises `stream`, reads the status word of `workspace` and returns
- * LCE_ERR_LABEL_RANGE if the most recent lce_forward / lce_backward that used
- * this workspace saw a bad label, LCE_OK otherwise.  Every call rewrites the
- * status word, so a fresh (uninitialised) workspace needs no clearing. */
+ * LCE_ERR_LABEL_RANGE if the most recent lce_forward / lce_backward /
+ * lce_forward_backward / KD call that used this workspace saw a bad label
+ * (under token parallelism: a bad label on ANY rank, so every rank reports
+ * it), else LCE_ERR_UPSTREAM if lce_expect_grad saw a mismatch since that
+ * call, else LCE_OK.  Every compute call rewrites the status word, so a fresh
+ * (uninitialised) workspace needs no clearing. */
 lce_status_t lce_check_device_status(void* workspace, void* stream);
+
+/* For callers (e.g. an autograd function) that ran lce_forward_backward with
+ * an assumed upstream gradient `expected` (the grad_loss it passed, 1 if NULL)
+ * and later receive the actual one as a device scalar `grad` [1] fp32: one
+ * tiny kernel compares them on the device (no host synchronisation) and, if
+ * they differ, sets a bit in the status word of `workspace` (the one the
+ * fused call used) so that lce_check_device_status returns LCE_ERR_UPSTREAM:
+ * the gradients already produced are then for the wrong scale.  Nothing is
+ * rescaled. */
+lce_status_t lce_expect_grad(const float* grad, float expected, void* workspace, void* stream);
 
 /* ---- communicator (vocab-parallel P:180 loss parallel, or token-parallel) --
  * Rank 0 creates a 128-byte id (host memory) and distributes it out of band
@@ -247,6 +285,11 @@ lce_status_t lce_comm_destroy(lce_comm_t comm);
 int lce_comm_size(lce_comm_t comm);
 int lce_comm_rank(lce_comm_t comm);
 int lce_comm_mode(lce_comm_t comm); /* lce_parallel_t; LCE_PAR_VOCAB for NULL */
+/* Polls ncclCommGetAsyncError: LCE_ERR_NCCL if the communicator hit an
+ * asynchronous error (a peer died, a network failure) -- the collectives of
+ * the calls above would otherwise block forever -- LCE_OK otherwise (also for
+ * NULL).  Host-only, no synchronisation; call it from a watchdog loop. */
+lce_status_t lce_comm_check(lce_comm_t comm);
 
 /* ---- introspection ------------------------------------------------------- */
 const char* lce_status_string(lce_status_t s);

@@ -12,6 +12,8 @@ from .lce_oracle import (  # noqa: F401
     lce_forward,
     lce_backward,
     lce_rows,
+    lce_lse,
+    lce_dweight_rows,
     shard_stats,
     shard_backward,
     combine_shard_stats,

@@ -47,6 +47,8 @@ __all__ = [
     "lce_forward",
     "lce_backward",
     "lce_rows",
+    "lce_lse",
+    "lce_dweight_rows",
     "shard_stats",
     "shard_backward",
     "combine_shard_stats",
@@ -191,6 +193,57 @@ def lce_rows(hidden, weight, labels, rows, n_valid: int,
         G[np.arange(sel.size), y[sel]] -= 1.0
         dH[sel] = (c if np.ndim(c) == 0 else c[:, None]) * (G @ W)
     return {"lse": lse, "token_loss": tok, "dH": dH}
+
+
+def lce_lse(hidden, weight, labels, ignore_index: int = IGNORE_INDEX, block: int = 1024) -> np.ndarray:
+    """Steps 1-3 for every row: lse_i = m_i + ln sum_j exp(z_ij - m_i) with
+    z_i = W h_i over the full vocabulary, 0 on ignored rows (R5).
+
+    Rows are taken ``block`` at a time only to bound host RAM (a [block, V]
+    fp64 logit slab); every row is still the textbook formula on its own.
+    """
+    W = _as_f64(weight)
+    hidden = np.asarray(hidden)
+    y = np.asarray(labels, dtype=np.int64)
+    valid = _valid_rows(y, W.shape[0], ignore_index)
+    rows = np.flatnonzero(valid)
+    lse = np.zeros(y.shape[0])
+    for a in range(0, rows.size, block):
+        r = rows[a:a + block]
+        _, lse[r] = _log_softmax_stats(_as_f64(hidden[r]) @ W.T)
+    return lse
+
+
+def lce_dweight_rows(hidden, weight, labels, vocab_rows, ignore_index: int = IGNORE_INDEX,
+                     reduction: str = "mean", grad_loss=1.0, lse=None) -> dict:
+    """Selected rows j of dW = G^T H (step 9) without forming all of G:
+
+        dW_j = sum_{i valid} c_i (exp(z_ij - lse_i) - [y_i = j]) h_i,   z_ij = h_i . w_j
+
+    which needs only the logit columns z[:, J] and each valid row's lse
+    (``lce_lse``, the oracle's own, unless the caller passes an oracle-made
+    one).  Used to check the GPU's dW at full size, where the whole oracle
+    backward would not fit in host memory; the cost is dominated by lse
+    (2 N_v V D flops).  Returns ``dW_rows`` [len(J), D] and ``lse`` [N].
+    """
+    H = np.asarray(hidden)
+    W = _as_f64(weight)
+    y = np.asarray(labels, dtype=np.int64)
+    J = np.asarray(vocab_rows, dtype=np.int64)
+    valid = _valid_rows(y, W.shape[0], ignore_index)
+    rows = np.flatnonzero(valid)
+    n_valid = int(rows.size)
+    c = _scale(reduction, n_valid, grad_loss, rows)
+    if lse is None:
+        lse = lce_lse(H, W, y, ignore_index)
+    dW = np.zeros((J.size, W.shape[1]))
+    if n_valid:
+        Hv = _as_f64(H[rows])
+        P = np.exp(Hv @ W[J].T - np.asarray(lse, dtype=np.float64)[rows][:, None])  # p_ij, j in J
+        P -= (y[rows][:, None] == J[None, :])                                           # - onehot
+        P *= c if np.ndim(c) == 0 else c[:, None]
+        dW = P.T @ Hv
+    return {"dW_rows": dW, "lse": np.asarray(lse, dtype=np.float64)}
 
 
 def shard_stats(hidden, weight_shard, labels, vocab_start: int, vocab_total: int,

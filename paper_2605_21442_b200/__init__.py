@@ -15,6 +15,7 @@ from .lce import (  # noqa: F401
     backward_adamw,
     check_device_status,
     debug_gemm,
+    expect_grad,
     forward,
     forward_backward,
     fused_workspace_bytes,

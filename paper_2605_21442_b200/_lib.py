@@ -19,8 +19,10 @@ KERNEL_CLASSES = ["prep", "gather", "fwd_gemm", "combine", "bwd_g", "bwd_dh", "b
 STATUS = {
     0: "LCE_OK", 1: "LCE_ERR_NULL", 2: "LCE_ERR_SHAPE", 3: "LCE_ERR_ALIGN", 4: "LCE_ERR_REDUCTION",
     5: "LCE_ERR_WORKSPACE", 6: "LCE_ERR_LABEL_RANGE", 7: "LCE_ERR_DEVICE", 8: "LCE_ERR_CUDA",
-    9: "LCE_ERR_NCCL", 10: "LCE_ERR_COMM",
+    9: "LCE_ERR_NCCL", 10: "LCE_ERR_COMM", 11: "LCE_ERR_ARG", 12: "LCE_ERR_UPSTREAM",
 }
+LCE_ERR_LABEL_RANGE, LCE_ERR_UPSTREAM = 6, 12
+LCE_DW_ACCUMULATE, LCE_DW_BF16 = 1, 2  # dweight_flags bits
 # Every symbol include/lce.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "lce_workspace_bytes", "lce_forward", "lce_backward", "lce_check_device_status",
@@ -29,7 +31,7 @@ EXPORTS = [
     "lce_status_string", "lce_abi_version", "lce_launch_count", "lce_profile_enable", "lce_profile_read",
     "lce_profile_read_clocks",
     "lce_debug_gemm", "lce_fused_workspace_bytes", "lce_forward_backward", "lce_backward_adamw",
-    "lce_kd_workspace_bytes", "lce_kd_forward_backward",
+    "lce_kd_workspace_bytes", "lce_kd_forward_backward", "lce_expect_grad", "lce_comm_check",
 ]
 
 
@@ -57,7 +59,7 @@ class Problem(ctypes.Structure):
     ]
 
 
-ABI_VERSION = 2  # include/lce.h LCE_ABI_VERSION
+ABI_VERSION = 3  # include/lce.h LCE_ABI_VERSION
 
 
 def _load() -> ctypes.CDLL:
@@ -93,6 +95,10 @@ def _load() -> ctypes.CDLL:
     lib.lce_kd_forward_backward.restype = ctypes.c_int
     lib.lce_check_device_status.argtypes = [vp, vp]
     lib.lce_check_device_status.restype = ctypes.c_int
+    lib.lce_expect_grad.argtypes = [vp, ctypes.c_float, vp, vp]
+    lib.lce_expect_grad.restype = ctypes.c_int
+    lib.lce_comm_check.argtypes = [vp]
+    lib.lce_comm_check.restype = ctypes.c_int
     lib.lce_comm_get_unique_id.argtypes = [ctypes.c_char_p]
     lib.lce_comm_get_unique_id.restype = ctypes.c_int
     lib.lce_comm_init.argtypes = [P(vp), ctypes.c_char_p, ctypes.c_int, ctypes.c_int]

@@ -14,6 +14,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 // the fp32 range); rows beyond it fall back to the tile-max form
 constexpr float kScaledQMax = 64.f;
 constexpr uint32_t kStatusBadLabel = 1u;
+constexpr uint32_t kStatusUpstream = 2u;  // lce_expect_grad saw a different upstream gradient
 
 // Device-side header at the start of the workspace.
 struct Header {
@@ -374,19 +375,33 @@ struct EpiDW : EpiBase {
     int32_t use_map;      // 1: write through `map` (fp32 32x32 boxes, 128B swizzle): TMA store,
                           //    or TMA reduce-add when accumulating (the L2 adds; no read by the SM)
     alignas(64) CUtensorMap map;  // [M rows of this GEMM, D] (rows / cols past it are clipped)
+    int32_t dbg;                  // A/B diagnostics: 1 skip the writes, 2 also the TMEM reads
+    uint16_t* dw_bf16;            // non-null: write bf16(c * acc) rows here instead (LCE_DW_BF16,
+                                  // overwrite only; the direct path)
+    int32_t prefetch;             // accumulate + TMA: L2 prefetch of the old dW rows
   };
   static __device__ __forceinline__ void finish(const Params& p) {
     if (p.use_map && (threadIdx.x & 31) == 0) tma_store_wait_all();
   }
-  // accumulate mode reads the old dW tile row: pull it into L2 while the MMA runs
+  // Accumulating (the fused path's later row chunks): the TMA reduce-add needs
+  // the old dW lines in L2; pull this tile's rows in (one bulk prefetch per
+  // row) while the MMA computes the tile, so the adds do not wait on HBM.
   static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
     const int r = t.m0 + t.row;
-    if (p.use_map || !p.accumulate || t.zero_acc || r >= t.M) return;
-    const float* row = p.dW + static_cast<int64_t>(r) * p.ld;
-    for (int c = 0; c < BN / 32 && t.n0 + 32 * c < t.N; ++c) prefetch_l2(row + t.n0 + 32 * c);
+    if (!p.use_map || !p.accumulate || !p.prefetch || t.zero_acc || r >= t.M || t.n0 >= t.N) return;
+    const int cols = min(BN, t.N - t.n0);
+    bulk_prefetch_l2(p.dW + static_cast<int64_t>(r) * p.ld + t.n0, static_cast<uint32_t>(cols * 4));
   }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     if (t.zero_acc && p.accumulate) return;  // K == 0 adds nothing (uniform across the CTA)
+    if (p.dbg) {
+      if (p.dbg == 1) {
+        float x[32];
+        for (int c = 0; c < BN / 32; ++c) load_chunk(taddr, c, false, x);
+        if (x[0] == 12345.f) *p.dW = x[1];  // keep the loads
+      }
+      return;
+    }
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const float cs = p.use_c ? p.hdr->c : 1.f;
@@ -414,26 +429,46 @@ struct EpiDW : EpiBase {
       }
       return;
     }
+    // Direct path: straight from registers to global memory (16-byte stores,
+    // or L2 reduce-adds when accumulating; bf16 rows for LCE_DW_BF16).
+    // Chunk c + 1's TMEM load is in flight while chunk c is written.
     float* row = p.dW + static_cast<int64_t>(r) * p.ld;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      float x[32];
-      load_chunk(taddr, c, t.zero_acc, x);
-      const int cb = t.n0 + c * 32;
-      if (!valid) continue;
+    uint16_t* brow = p.dw_bf16 ? p.dw_bf16 + static_cast<int64_t>(r) * p.ld : nullptr;
+    uint32_t v[2][32];
+    tmem_ld32(taddr, v[0]);
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        const int col = cb + 4 * v;
-        if (col >= t.N) break;
-        float4 a = make_float4(cs * x[4 * v], cs * x[4 * v + 1], cs * x[4 * v + 2], cs * x[4 * v + 3]);
-        if (p.accumulate) {
-          const float4 o = *reinterpret_cast<const float4*>(row + col);
-          a.x += o.x;
-          a.y += o.y;
-          a.z += o.z;
-          a.w += o.w;
+    for (int c = 0; c < BN / 32; ++c) {
+      tmem_ld_wait();
+      if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+      const uint32_t* u = v[c & 1];
+      const int cb = t.n0 + c * 32;
+      if (!valid || cb >= t.N) continue;
+      if (brow) {  // D % 8 == 0: a group of 8 columns is either all in range or all out
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = cb + 8 * q;
+          if (col >= t.N) break;
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            w[e] = t.zero_acc ? 0u
+                              : pack_bf16x2(cs * __uint_as_float(u[8 * q + 2 * e]),
+                                            cs * __uint_as_float(u[8 * q + 2 * e + 1]));
+          *reinterpret_cast<uint4*>(brow + col) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        *reinterpret_cast<float4*>(row + col) = a;
+        continue;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int col = cb + 4 * q;
+        if (col >= t.N) break;
+        float a[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[e] = t.zero_acc ? 0.f : cs * __uint_as_float(u[4 * q + e]);
+        if (p.accumulate)
+          red_add_v4(row + col, a[0], a[1], a[2], a[3]);
+        else
+          st_global_v4(row + col, a[0], a[1], a[2], a[3]);
       }
     }
   }
@@ -651,9 +686,16 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
 // to the full batch's.
 __global__ void tp_scale_kernel(Header* hdr, const float* __restrict__ grad_loss, int reduction) {
   const int nv = hdr->tp_nv;
+  // a bad label on any rank poisons the summed loss on every rank: report it on every rank too
+  if (hdr->tp_bad) hdr->status |= kStatusBadLabel;
   const float g = (grad_loss && reduction != 2) ? *grad_loss : 1.f;
   hdr->mean_div = nv;
   if (hdr->n_valid > 0 && reduction == 0) hdr->c = nv == 0 ? 0.f : g / static_cast<float>(nv);
+}
+
+// lce_expect_grad: the upstream gradient the fused call assumed vs the actual one.
+__global__ void expect_grad_kernel(const float* __restrict__ grad, float expected, Header* hdr) {
+  if (*grad != expected) hdr->status |= kStatusUpstream;
 }
 
 // ============================================================ S0 gather

@@ -114,7 +114,11 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
 // path keeps fp32 logits for student and teacher (see KdPlan).
 constexpr int64_t kDefaultFusedBudget = 2ll << 30;
 constexpr int64_t kDefaultKdBudget = 4ll << 30;
-constexpr int kPlanSms = 148;  // B200: the split-K choice is made at plan time (host-pure sizes)
+// Workspace sizes are host-pure, so the plan assumes a full B200 (148 SMs) when
+// it reserves the dH split-K slabs; at launch the split factor and tile shape
+// are re-derived from the current device's SM count (fit_plan_to_device),
+// capped by the slab space reserved here.
+constexpr int kPlanSms = 148;
 // dH / dW GEMMs use 512 x 256 wide pair tiles when the token rows they reduce
 // over (the fused row chunk, or all tokens in the recompute path) number at
 // least this many: shorter k-ranges leave the epilogue of the wide kernel's
@@ -125,6 +129,7 @@ constexpr int64_t kWideMinDhK = 12288;
 struct FusedPlan {
   int64_t N, D, Vl, cap, ldv, n_tiles, Nc, n_chunks;
   int split;                       // split-K factor of the chunk's dH GEMM
+  int split_cap;                   // largest split the reserved slab space holds
   int wide_dh, wide_dw;            // 512 x 256 tiles for the chunk's dH / dW GEMMs
   size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, slab;
   size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
@@ -160,6 +165,20 @@ int dh_split(int64_t Nc, int64_t D, int max_split, int sms, int64_t rows) {
   return best;
 }
 
+// Tile shape and split-K factor of a fused row chunk's dH GEMM (and the dW
+// tile shape) for a grid of `sms` SMs.
+void choose_dh(FusedPlan* q, int max_split, int sms) {
+  const int split_wide = dh_split(q->Nc, q->D, max_split, sms, kWideBM);
+  q->wide_dh = use_pair() && use_wide(LCE_K_BWD_DH, (q->Nc >= kWideMinRows && q->Vl / split_wide >= kWideMinDhK) ? 1 : 0);
+  q->wide_dw = use_pair() && use_wide(LCE_K_BWD_DW, q->Nc >= kWideMinRows ? 1 : 0);
+  q->split = dh_split(q->Nc, q->D, max_split, sms, !use_pair() ? BM : (q->wide_dh ? kWideBM : kPairBM));
+}
+
+// The plan was made for kPlanSms; re-derive the dH schedule for this device.
+void fit_plan_to_device(FusedPlan* q, int sms) {
+  if (sms != kPlanSms) choose_dh(q, q->split_cap, sms);
+}
+
 // kd: student chunk keeps fp32 Z + bf16 G (6 bytes per element), the dH
 // split-K slabs alias Z; otherwise the CE layout above with its own slabs.
 bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
@@ -190,10 +209,8 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   // pair tiles were 5% faster per step, at P = 4 (16,032) and P = 2 (32,064)
   // wide tiles 1-4% faster)
   const int max_split = kd ? static_cast<int>(q.ldv / q.D) : 8;
-  const int split_wide = dh_split(q.Nc, q.D, max_split, kPlanSms, kWideBM);
-  q.wide_dh = use_pair() && use_wide(LCE_K_BWD_DH, (q.Nc >= kWideMinRows && q.Vl / split_wide >= kWideMinDhK) ? 1 : 0);
-  q.wide_dw = use_pair() && use_wide(LCE_K_BWD_DW, q.Nc >= kWideMinRows ? 1 : 0);
-  q.split = dh_split(q.Nc, q.D, max_split, kPlanSms, !use_pair() ? BM : (q.wide_dh ? kWideBM : kPairBM));
+  choose_dh(&q, max_split, kPlanSms);
+  q.split_cap = kd ? max_split : q.split;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
@@ -458,6 +475,20 @@ int z_tma() {
   const char* e = getenv("LCE_ZSTORE");
   return (e && strcmp(e, "direct") == 0) ? 0 : 1;
 }
+// dW epilogue: fp32 rows staged in shared memory and written with TMA stores /
+// reduce-adds (default), or (LCE_DW_STORE=direct) straight from registers
+// (16-byte st.global / red.global.add.v4.f32).  Measured on B200 (8B / 1B /
+// 70B fused, 8B split): the direct path was 1-6% slower per dW launch.
+int dw_tma() {
+  const char* e = getenv("LCE_DW_STORE");
+  return (e && strcmp(e, "direct") == 0) ? 0 : 1;
+}
+// Diagnostics (A/B only): LCE_DBG_EPI=1 makes the dW epilogue skip its global
+// writes, =2 also its TMEM reads (the mainloop alone); results are then wrong.
+int dbg_epi() {
+  const char* e = getenv("LCE_DBG_EPI");
+  return e ? atoi(e) : 0;
+}
 
 // Rows of the TMA box of a K-major B operand: each CTA of a pair stages half of
 // the 256-column tile.
@@ -556,6 +587,7 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
   ncclResult_t (*groupStart)();
   ncclResult_t (*groupEnd)();
+  ncclResult_t (*getAsyncError)(ncclComm_t, ncclResult_t*);
 };
 
 NcclApi* nccl() {
@@ -573,6 +605,7 @@ NcclApi* nccl() {
     api.allReduce = reinterpret_cast<decltype(api.allReduce)>(dlsym(h, "ncclAllReduce"));
     api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
     api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.getAsyncError = reinterpret_cast<decltype(api.getAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
   });
   return api.ok ? &api : nullptr;
@@ -692,6 +725,8 @@ const char* lce_status_string(lce_status_t s) {
     case LCE_ERR_CUDA: return "CUDA error";
     case LCE_ERR_NCCL: return "NCCL error or NCCL unavailable";
     case LCE_ERR_COMM: return "communicator does not match problem";
+    case LCE_ERR_ARG: return "unsupported flag combination";
+    case LCE_ERR_UPSTREAM: return "upstream gradient differs from the one the fused call assumed";
   }
   return "unknown status";
 }
@@ -810,15 +845,22 @@ struct AdamArgs {
 
 lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden, const uint16_t* weight,
                            const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
-                           float* dweight, int accumulate_dweight, const AdamArgs* adam, void* workspace,
+                           void* dweight_out, int dweight_flags, const AdamArgs* adam, void* workspace,
                            size_t workspace_bytes, void* stream) {
   Plan pl;
   LCE_TRY(validate(p, comm_in, workspace_bytes, workspace, &pl));
   lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
   if (tp && adam) return LCE_ERR_COMM;  // the in-backward step needs the full-batch dW
-  if (!weight || (!dweight && !adam)) return LCE_ERR_NULL;
+  if ((dweight_flags & ~(LCE_DW_ACCUMULATE | LCE_DW_BF16)) ||
+      ((dweight_flags & LCE_DW_BF16) && (dweight_flags & LCE_DW_ACCUMULATE)))
+    return LCE_ERR_ARG;
+  const bool accumulate_dweight = (dweight_flags & LCE_DW_ACCUMULATE) != 0;
+  const bool dw_bf16 = (dweight_flags & LCE_DW_BF16) != 0;
+  float* dweight = dw_bf16 ? nullptr : static_cast<float*>(dweight_out);
+  uint16_t* dweight_h = dw_bf16 ? static_cast<uint16_t*>(dweight_out) : nullptr;
+  if (!weight || (!dweight_out && !adam)) return LCE_ERR_NULL;
   if (pl.N > 0 && (!hidden || !labels || !lse || !dhidden)) return LCE_ERR_NULL;
-  const void* ptrs[] = {hidden, weight, labels, lse, grad_loss, dhidden, dweight};
+  const void* ptrs[] = {hidden, weight, labels, lse, grad_loss, dhidden, dweight_out};
   for (const void* q : ptrs)
     if (q && !aligned16(q)) return LCE_ERR_ALIGN;
   DevInfo dev;
@@ -828,7 +870,8 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
   Header* hdr = reinterpret_cast<Header*>(ws + pl.hdr);
 
   if (pl.N == 0 && !adam) {
-    if (!accumulate_dweight) LCE_CUDA(cudaMemsetAsync(dweight, 0, pl.Vl * pl.D * sizeof(float), s));
+    if (!accumulate_dweight)
+      LCE_CUDA(cudaMemsetAsync(dweight_out, 0, pl.Vl * pl.D * (dw_bf16 ? sizeof(uint16_t) : sizeof(float)), s));
     if (tp) return tp_empty_rank(tp, p, hdr, grad_loss, nullptr, nullptr, s);
     return LCE_OK;
   }
@@ -922,9 +965,13 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
     {
       GemmDims d{nullptr, static_cast<int32_t>(vc), &hdr->n_valid, 0, static_cast<int32_t>(pl.D)};
       if (!adam) {
-        EpiDW::Params ep{dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
-        ep.use_map = z_tma();
+        EpiDW::Params ep{dw_bf16 ? nullptr : dweight + v0 * pl.D, pl.D, accumulate_dweight ? 1 : 0, hdr, 1};
+        // bf16 rows are written straight from registers (the direct epilogue)
+        ep.use_map = dw_bf16 ? 0 : dw_tma();
+        ep.dw_bf16 = dw_bf16 ? dweight_h + v0 * pl.D : nullptr;
+        ep.dbg = dbg_epi();
         if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight + v0 * pl.D, pl.D, vc, pl.D));
+        ep.prefetch = 0;  // each dW row block is written once here (K = all tokens)
         // the last chunk's dW runs beside the dH all-reduce (vocab-parallel)
         const int g_sms = (multi && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
         LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, g_sms, s,
@@ -988,7 +1035,9 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
   {
     GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
     EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
-    ep.use_map = z_tma();
+    ep.use_map = dw_tma();
+    ep.dbg = dbg_epi();
+    ep.prefetch = !(getenv("LCE_DW_PREFETCH") && atoi(getenv("LCE_DW_PREFETCH")) == 0);
     if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
     // runs beside this chunk's dH all-reduce under vocab parallelism
     LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, overlap_sms(comm, sms), s,
@@ -1010,9 +1059,9 @@ extern "C" {
 
 lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_t* hidden, const uint16_t* weight,
                           const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
-                          float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
+                          void* dweight, int dweight_flags, void* workspace, size_t workspace_bytes,
                           void* stream) {
-  return backward_impl(p, comm, hidden, weight, labels, lse, grad_loss, dhidden, dweight, accumulate_dweight, nullptr,
+  return backward_impl(p, comm, hidden, weight, labels, lse, grad_loss, dhidden, dweight, dweight_flags, nullptr,
                        workspace, workspace_bytes, stream);
 }
 
@@ -1039,9 +1088,11 @@ size_t lce_fused_workspace_bytes(const lce_problem_t* p) {
 lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden,
                                   const uint16_t* weight, const int32_t* labels, const float* grad_loss,
                                   float* loss, float* lse, float* token_loss, int32_t* n_valid, uint16_t* dhidden,
-                                  float* dweight, int accumulate_dweight, void* workspace, size_t workspace_bytes,
+                                  float* dweight, int dweight_flags, void* workspace, size_t workspace_bytes,
                                   void* stream) {
   if (!p) return LCE_ERR_NULL;
+  if (dweight_flags & ~LCE_DW_ACCUMULATE) return LCE_ERR_ARG;  // fp32 only: dW is summed over row chunks
+  const bool accumulate_dweight = dweight_flags != 0;
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   FusedPlan fp;
   if (!make_fused_plan(p, &fp)) return LCE_ERR_SHAPE;
@@ -1055,6 +1106,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   if (workspace_bytes < fp.total) return LCE_ERR_WORKSPACE;
   DevInfo dev;
   LCE_TRY(device_info(&dev));
+  fit_plan_to_device(&fp, dev.sms);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
@@ -1220,9 +1272,11 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in,
                                      const uint16_t* hidden_s, const uint16_t* weight_s, const uint16_t* hidden_t,
                                      const uint16_t* weight_t, const int32_t* labels, const float* grad_loss,
                                      float* loss, float* token_loss, int32_t* n_valid, uint16_t* dhidden_s,
-                                     float* dweight_s, int accumulate_dweight, void* workspace,
+                                     float* dweight_s, int dweight_flags, void* workspace,
                                      size_t workspace_bytes, void* stream) {
   if (!p) return LCE_ERR_NULL;
+  if (dweight_flags & ~LCE_DW_ACCUMULATE) return LCE_ERR_ARG;  // fp32 only: dW is summed over row chunks
+  const bool accumulate_dweight = dweight_flags != 0;
   if (p->reduction != LCE_MEAN && p->reduction != LCE_SUM && p->reduction != LCE_NONE) return LCE_ERR_REDUCTION;
   KdPlan kp;
   if (!make_kd_plan(p, teacher_dim, &kp)) return LCE_ERR_SHAPE;
@@ -1238,6 +1292,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in,
   if (workspace_bytes < kp.total) return LCE_ERR_WORKSPACE;
   DevInfo dev;
   LCE_TRY(device_info(&dev));
+  fit_plan_to_device(&kp.f, dev.sms);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   Header* hdr = reinterpret_cast<Header*>(ws + fp.hdr);
@@ -1377,7 +1432,19 @@ lce_status_t lce_check_device_status(void* workspace, void* stream) {
   LCE_CUDA(cudaMemcpyAsync(&h, workspace, sizeof(Header), cudaMemcpyDeviceToHost, s));
   LCE_CUDA(cudaStreamSynchronize(s));
   if (h.status & kStatusBadLabel) return LCE_ERR_LABEL_RANGE;
+  if (h.status & kStatusUpstream) return LCE_ERR_UPSTREAM;
   return LCE_OK;
+}
+
+lce_status_t lce_expect_grad(const float* grad, float expected, void* workspace, void* stream) {
+  if (!grad || !workspace) return LCE_ERR_NULL;
+  if (!aligned16(workspace)) return LCE_ERR_ALIGN;
+  DevInfo dev;
+  LCE_TRY(device_info(&dev));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LaunchScope sc(LCE_K_FINAL, s);
+  expect_grad_kernel<<<1, 1, 0, s>>>(grad, expected, static_cast<Header*>(workspace));
+  return last_error();
 }
 
 lce_status_t lce_comm_get_unique_id(uint8_t id[128]) {
@@ -1432,6 +1499,15 @@ lce_status_t lce_comm_destroy(lce_comm_t comm) {
 int lce_comm_size(lce_comm_t comm) { return comm ? comm->nranks : 1; }
 int lce_comm_rank(lce_comm_t comm) { return comm ? comm->rank : 0; }
 int lce_comm_mode(lce_comm_t comm) { return comm ? comm->mode : LCE_PAR_VOCAB; }
+
+lce_status_t lce_comm_check(lce_comm_t comm) {
+  if (!comm) return LCE_OK;
+  NcclApi* api = nccl();
+  if (!api || !api->getAsyncError) return LCE_ERR_NCCL;
+  ncclResult_t r = ncclSuccess;
+  if (api->getAsyncError(comm->comm, &r) != ncclSuccess) return LCE_ERR_NCCL;
+  return (r == ncclSuccess || r == ncclInProgress) ? LCE_OK : LCE_ERR_NCCL;
+}
 
 lce_status_t lce_profile_enable(int on) {
   std::lock_guard<std::mutex> lk(g_prof.mu);

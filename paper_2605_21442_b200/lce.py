@@ -13,7 +13,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import KERNEL_CLASSES, LCE_K_COUNT, AdamW, Problem, check, lib
+from ._lib import LCE_DW_ACCUMULATE, LCE_DW_BF16, KERNEL_CLASSES, LCE_K_COUNT, AdamW, Problem, check, lib
 from .dist import broadcast_bytes, shard_range  # noqa: F401
 
 MEAN, SUM, NONE = 0, 1, 2
@@ -68,14 +68,50 @@ def _ws_for(ws: Optional[Workspace], problem: Problem, device) -> torch.Tensor:
     return ws.get(need, device)
 
 
+def _check_tensor(t: Optional[torch.Tensor], name: str, dtype, shape: tuple, device) -> None:
+    """Every tensor handed to the C ABI: dtype, exact shape, device, dense.
+    The library builds its TMA maps and grids from the problem's N / D / V_l,
+    so a mismatched buffer would be read or written out of bounds."""
+    if t is None:
+        return
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_cuda or t.device != device:
+        raise ValueError(f"{name} must live on {device}, got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
 def _check_inputs(hidden, weight, labels):
-    if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
-        raise TypeError("hidden and weight must be bf16")
-    if labels.dtype != torch.int32:
-        raise TypeError("labels must be int32")
-    for t in (hidden, weight, labels):
-        if not t.is_cuda or not t.is_contiguous():
-            raise ValueError("tensors must be contiguous CUDA tensors")
+    """hidden [N, D] bf16, weight [V_l, D] bf16, labels [N] int32, one CUDA device."""
+    if hidden.dim() != 2 or weight.dim() != 2:
+        raise ValueError("hidden must be [N, D] and weight [V_l, D]")
+    N, D = hidden.shape
+    dev = hidden.device
+    _check_tensor(hidden, "hidden", torch.bfloat16, (N, D), dev)
+    _check_tensor(weight, "weight", torch.bfloat16, (weight.shape[0], D), dev)
+    _check_tensor(labels, "labels", torch.int32, (N,), dev)
+    return N, D, weight.shape[0]
+
+
+def _grad_input(grad_loss, n: int, device) -> Optional[torch.Tensor]:
+    """The upstream gradient as the device fp32 vector the ABI takes: [N] for
+    'none', [1] otherwise (input marshalling; None means 1)."""
+    if grad_loss is None:
+        return None
+    g = torch.as_tensor(grad_loss).to(device=device, dtype=torch.float32).reshape(-1).contiguous()
+    if g.numel() != n:
+        raise ValueError(f"grad_loss must have {n} element(s) (N for 'none', 1 otherwise), got {g.numel()}")
+    return g
+
+
+def _check_out(out: dict, N: int, dev) -> None:
+    _check_tensor(out.get("loss"), "out['loss']", torch.float32, (1,), dev)
+    _check_tensor(out.get("lse"), "out['lse']", torch.float32, (N,), dev)
+    _check_tensor(out.get("n_valid"), "out['n_valid']", torch.int32, (1,), dev)
+    _check_tensor(out.get("token_loss"), "out['token_loss']", torch.float32, (N,), dev)
 
 
 PARALLEL_MODES = {"vocab": 0, "token": 1}  # lce_parallel_t
@@ -119,6 +155,11 @@ class Comm:
               "lce_comm_init_mode")
         return cls(h, 1, 0, mode)
 
+    def check(self) -> None:
+        """lce_comm_check: raises LceError(LCE_ERR_NCCL) if NCCL reported an
+        asynchronous error on this communicator (host only, no sync)."""
+        check(lib.lce_comm_check(self.handle), "lce_comm_check")
+
     def close(self):
         if self.handle:
             check(lib.lce_comm_destroy(self.handle), "lce_comm_destroy")
@@ -134,9 +175,8 @@ def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *,
     reduction 'none' returns the per-token losses (-log p(y_i)) in token_loss
     and their sum in loss."""
     with_token_loss = with_token_loss or reduction == "none"
-    _check_inputs(hidden, weight, labels)
-    N, D = hidden.shape
-    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+    N, D, Vl = _check_inputs(hidden, weight, labels)
+    prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
     ws = _ws_for(workspace, prob, dev)
@@ -147,6 +187,7 @@ def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *,
             "n_valid": torch.empty(1, dtype=torch.int32, device=dev),
             "token_loss": torch.empty(N, dtype=torch.float32, device=dev) if with_token_loss else None,
         }
+    _check_out(out, N, dev)
     check(lib.lce_forward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
                           _ptr(labels), _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["token_loss"]),
                           _ptr(out["n_valid"]), _ptr(ws), ws.numel(), _stream(stream)), "lce_forward")
@@ -158,27 +199,32 @@ def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, l
              comm: Optional[Comm] = None, vocab_start: int = 0, vocab_total: Optional[int] = None,
              dhidden: Optional[torch.Tensor] = None, dweight: Optional[torch.Tensor] = None,
              accumulate_dweight: bool = False, workspace: Optional[Workspace] = None, chunk_budget_bytes: int = 0,
-             stream=None):
-    """dhidden [N, D] bf16 and dweight [V_l, D] fp32 (overwritten or accumulated).
+             stream=None, dweight_dtype=torch.float32):
+    """dhidden [N, D] bf16 and dweight [V_l, D] (overwritten or accumulated).
 
-    grad_loss: scalar dL/dloss for 'mean'/'sum'; [N] per-token dL/dloss_i for 'none'."""
-    _check_inputs(hidden, weight, labels)
-    N, D = hidden.shape
-    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+    grad_loss: scalar dL/dloss for 'mean'/'sum'; [N] per-token dL/dloss_i for 'none'.
+    dweight_dtype: torch.float32 (default), or torch.bfloat16 -- the library
+    rounds the fp32 accumulator to bf16 itself (LCE_DW_BF16; not with
+    accumulate_dweight)."""
+    N, D, Vl = _check_inputs(hidden, weight, labels)
+    if dweight_dtype not in (torch.float32, torch.bfloat16):
+        raise TypeError("dweight_dtype must be torch.float32 or torch.bfloat16")
+    prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
+    _check_tensor(lse, "lse", torch.float32, (N,), dev)
     ws = _ws_for(workspace, prob, dev)
     if dhidden is None:
         dhidden = torch.empty_like(hidden)
     if dweight is None:
-        dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
-    if grad_loss is not None:
-        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
-        if grad_loss.numel() != (N if reduction == "none" else 1):
-            raise ValueError("grad_loss must have N elements for 'none' and 1 otherwise")
+        dweight = torch.empty(weight.shape, dtype=dweight_dtype, device=dev)
+    _check_tensor(dhidden, "dhidden", torch.bfloat16, (N, D), dev)
+    _check_tensor(dweight, "dweight", dweight_dtype, (Vl, D), dev)
+    grad_loss = _grad_input(grad_loss, N if reduction == "none" else 1, dev)
+    flags = (LCE_DW_ACCUMULATE if accumulate_dweight else 0) | (LCE_DW_BF16 if dweight_dtype == torch.bfloat16 else 0)
     check(lib.lce_backward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
                            _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(dweight),
-                           1 if accumulate_dweight else 0, _ptr(ws), ws.numel(), _stream(stream)), "lce_backward")
+                           flags, _ptr(ws), ws.numel(), _stream(stream)), "lce_backward")
     return dhidden, dweight
 
 
@@ -192,19 +238,18 @@ def backward_adamw(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Ten
     """lce_backward with the LM-head AdamW step fused into the dW epilogue
     (optimizer-in-backward).  Updates weight (bf16), master_weight,
     exp_avg, exp_avg_sq in place; returns dhidden."""
-    _check_inputs(hidden, weight, labels)
-    for t in (master_weight, exp_avg, exp_avg_sq):
-        if t.dtype != torch.float32 or t.shape != weight.shape or not t.is_contiguous():
-            raise ValueError("master_weight / exp_avg / exp_avg_sq must be contiguous fp32 like weight")
-    N, D = hidden.shape
-    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
-                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
+    N, D, Vl = _check_inputs(hidden, weight, labels)
     dev = hidden.device
+    for name, t in (("master_weight", master_weight), ("exp_avg", exp_avg), ("exp_avg_sq", exp_avg_sq)):
+        _check_tensor(t, name, torch.float32, (Vl, D), dev)
+    _check_tensor(lse, "lse", torch.float32, (N,), dev)
+    prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
+                        ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     ws = _ws_for(workspace, prob, dev)
     if dhidden is None:
         dhidden = torch.empty_like(hidden)
-    if grad_loss is not None:
-        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+    _check_tensor(dhidden, "dhidden", torch.bfloat16, (N, D), dev)
+    grad_loss = _grad_input(grad_loss, N if reduction == "none" else 1, dev)
     hp = AdamW(lr, betas[0], betas[1], eps, weight_decay, step)
     check(lib.lce_backward_adamw(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
                                  _ptr(labels), _ptr(lse), _ptr(grad_loss), _ptr(dhidden), _ptr(master_weight),
@@ -226,10 +271,11 @@ def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.T
                      vocab_total: Optional[int] = None) -> dict:
     """Fused forward + backward without logit recompute (lce_forward_backward).
 
-    Returns {loss, lse, n_valid, token_loss, dhidden, dweight}."""
-    _check_inputs(hidden, weight, labels)
-    N, D = hidden.shape
-    prob = make_problem(N, D, weight.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+    Returns {loss, lse, n_valid, token_loss, dhidden, dweight}; dweight is fp32
+    (summed over row chunks).  grad_loss (the upstream gradient) must be known
+    up front: scalar for 'mean'/'sum', [N] for 'none'; None = 1."""
+    N, D, Vl = _check_inputs(hidden, weight, labels)
+    prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
     need = fused_workspace_bytes(prob)
@@ -250,10 +296,10 @@ def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.T
         dhidden = torch.empty_like(hidden)
     if dweight is None:
         dweight = torch.empty(weight.shape, dtype=torch.float32, device=dev)
-    if grad_loss is not None:
-        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
-        if grad_loss.numel() != (N if reduction == "none" else 1):
-            raise ValueError("grad_loss must have N elements for 'none' and 1 otherwise")
+    _check_out(out, N, dev)
+    _check_tensor(dhidden, "dhidden", torch.bfloat16, (N, D), dev)
+    _check_tensor(dweight, "dweight", torch.float32, (Vl, D), dev)
+    grad_loss = _grad_input(grad_loss, N if reduction == "none" else 1, dev)
     check(lib.lce_forward_backward(ctypes.byref(prob), comm.handle if comm else None, _ptr(hidden), _ptr(weight),
                                    _ptr(labels),
                                    _ptr(grad_loss), _ptr(out["loss"]), _ptr(out["lse"]), _ptr(out["token_loss"]),
@@ -273,13 +319,11 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
                         vocab_total: Optional[int] = None) -> dict:
     """Linear KD loss (forward KL, teacher -> student) and student gradients
     (lce_kd_forward_backward).  Returns {loss, token_loss, n_valid, dhidden, dweight}."""
-    _check_inputs(hidden_s, weight_s, labels)
-    _check_inputs(hidden_t, weight_t, labels)
-    N, D = hidden_s.shape
-    Dt = hidden_t.shape[1]
-    if hidden_t.shape[0] != N or weight_t.shape[0] != weight_s.shape[0]:
+    N, D, Vl = _check_inputs(hidden_s, weight_s, labels)
+    Nt, Dt, Vt = _check_inputs(hidden_t, weight_t, labels)
+    if Nt != N or Vt != Vl or hidden_t.device != hidden_s.device:
         raise ValueError("teacher / student shapes disagree")
-    prob = make_problem(N, D, weight_s.shape[0], vocab_start=vocab_start, vocab_total=vocab_total,
+    prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden_s.device
     need = int(lib.lce_kd_workspace_bytes(ctypes.byref(prob), Dt))
@@ -295,8 +339,9 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
         dhidden = torch.empty_like(hidden_s)
     if dweight is None:
         dweight = torch.empty(weight_s.shape, dtype=torch.float32, device=dev)
-    if grad_loss is not None:
-        grad_loss = grad_loss.to(device=dev, dtype=torch.float32).contiguous()
+    _check_tensor(dhidden, "dhidden", torch.bfloat16, (N, D), dev)
+    _check_tensor(dweight, "dweight", torch.float32, (Vl, D), dev)
+    grad_loss = _grad_input(grad_loss, N if reduction == "none" else 1, dev)
     check(lib.lce_kd_forward_backward(ctypes.byref(prob), comm.handle if comm else None, Dt, _ptr(hidden_s),
                                       _ptr(weight_s), _ptr(hidden_t),
                                       _ptr(weight_t), _ptr(labels), _ptr(grad_loss), _ptr(out["loss"]),
@@ -308,15 +353,34 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
 
 
 def check_device_status(workspace: Optional[Workspace] = None, device=None, stream=None) -> None:
-    """Raises LceError(LCE_ERR_LABEL_RANGE) if a bad label was seen (syncs)."""
-    ws = workspace or _default_ws.get(str(device or torch.device("cuda", torch.cuda.current_device())))
-    if ws is None or ws.buf is None:
-        return
-    check(lib.lce_check_device_status(_ptr(ws.buf), _stream(stream)), "lce_check_device_status")
+    """Raises LceError(LCE_ERR_LABEL_RANGE) if a bad label was seen, or
+    LceError(LCE_ERR_UPSTREAM) if a fused autograd call's upstream gradient
+    differed from the one it assumed (syncs).  Without `workspace`, checks
+    every default workspace of the device (split, fused and KD paths)."""
+    if workspace is not None:
+        wss = [workspace]
+    else:
+        dev = str(device or torch.device("cuda", torch.cuda.current_device()))
+        wss = [w for k, w in _default_ws.items() if k == dev or k.startswith(dev + ":")]
+    for ws in wss:
+        if ws.buf is not None:
+            check(lib.lce_check_device_status(_ptr(ws.buf), _stream(stream)), "lce_check_device_status")
+
+
+def expect_grad(grad: torch.Tensor, expected: float, workspace: Workspace, stream=None) -> None:
+    """lce_expect_grad: compare the actual upstream gradient (device [1] fp32)
+    with the one a fused call assumed, on the device, no sync; a mismatch is
+    raised by the next check_device_status as LCE_ERR_UPSTREAM."""
+    _check_tensor(grad, "grad", torch.float32, (1,), grad.device)
+    check(lib.lce_expect_grad(_ptr(grad), float(expected), _ptr(workspace.buf), _stream(stream)), "lce_expect_grad")
 
 
 class LinearCrossEntropyFunction(torch.autograd.Function):
-    """autograd wrapper: loss = CE(hidden @ weight^T, labels), mask-first, chunked."""
+    """autograd wrapper: loss = CE(hidden @ weight^T, labels), mask-first, chunked.
+
+    backward passes autograd's upstream gradient to lce_backward as grad_loss
+    and asks the library for dW in the weight's dtype (bf16: LCE_DW_BF16, the
+    library rounds its fp32 accumulator); nothing is computed here."""
 
     @staticmethod
     def forward(ctx, hidden, weight, labels, ignore_index, reduction):
@@ -331,40 +395,55 @@ class LinearCrossEntropyFunction(torch.autograd.Function):
     def backward(ctx, g):
         hidden, weight, labels, lse = ctx.saved_tensors
         ignore_index, reduction = ctx.cfg
-        dh, dw = backward(hidden, weight, labels, lse, grad_loss=g.reshape(-1), ignore_index=ignore_index,
-                          reduction=reduction)
-        return dh, dw.to(weight.dtype), None, None, None
+        dh, dw = backward(hidden, weight, labels, lse, grad_loss=g, ignore_index=ignore_index,
+                          reduction=reduction, dweight_dtype=weight.dtype)
+        return dh, dw, None, None, None
 
 
 class LinearCrossEntropyFusedFunction(torch.autograd.Function):
-    """autograd wrapper over lce_forward_backward: the gradients for an upstream
-    gradient of 1 are produced together with the loss (no logit recompute) and
-    scaled by the actual upstream scalar in backward (MEAN / SUM are linear in it)."""
+    """autograd wrapper over lce_forward_backward (no logit recompute).
+
+    The fused call needs the upstream gradient before the backward exists, so
+    the caller states it up front as `grad_scale` (1.0 for loss.backward();
+    e.g. 1/k when the loss is divided by k for gradient accumulation): it is
+    passed to the library as grad_loss and the gradients come out for it.
+    backward returns them untouched -- dW in fp32, as lce_forward_backward
+    sums it over row chunks (autograd's engine stores it in the parameter's
+    dtype) -- and hands the actual upstream gradient to lce_expect_grad, which
+    compares it with grad_scale on the device: a mismatch surfaces as
+    LCE_ERR_UPSTREAM from check_device_status.  No rescaling, no host sync."""
 
     @staticmethod
-    def forward(ctx, hidden, weight, labels, ignore_index, reduction):
-        out = forward_backward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)
+    def forward(ctx, hidden, weight, labels, ignore_index, reduction, grad_scale):
+        dev = hidden.device
+        ws = _default_ws.setdefault(str(dev) + ":fused", Workspace())
+        g = torch.full((1,), float(grad_scale), dtype=torch.float32, device=dev)
+        out = forward_backward(hidden, weight, labels, grad_loss=g, ignore_index=ignore_index, reduction=reduction,
+                               workspace=ws)
         ctx.save_for_backward(out["dhidden"], out["dweight"])
-        ctx.wdtype = weight.dtype
+        ctx.ws, ctx.scale = ws, float(grad_scale)
         return out["loss"].reshape(())
 
     @staticmethod
     def backward(ctx, g):
         dh, dw = ctx.saved_tensors
-        if not torch.equal(g, torch.ones_like(g)):  # the common loss.backward() case needs no rescale
-            dh = (dh.float() * g).to(dh.dtype)
-            dw = dw * g
-        return dh, dw.to(ctx.wdtype), None, None, None
+        expect_grad(g.reshape(1), ctx.scale, ctx.ws)
+        return dh, dw, None, None, None, None
 
 
 def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduction: str = "mean",
-                         fused: bool = False):
+                         fused: bool = False, grad_scale: float = 1.0):
     """loss = CE(hidden @ weight^T, labels) (P:166 LCE).  fused=True computes the
-    gradients in the forward call without the logit recompute (MEAN / SUM only)."""
+    gradients in the forward call without the logit recompute (MEAN / SUM only),
+    for the upstream gradient `grad_scale`; when no gradient is needed
+    (torch.no_grad(), or neither hidden nor weight requires grad) it runs the
+    forward only."""
     if fused:
         if reduction == "none":
             raise ValueError("fused autograd needs a scalar loss (reduction 'mean' or 'sum')")
-        return LinearCrossEntropyFusedFunction.apply(hidden, weight, labels, ignore_index, reduction)
+        if torch.is_grad_enabled() and (hidden.requires_grad or weight.requires_grad):
+            return LinearCrossEntropyFusedFunction.apply(hidden, weight, labels, ignore_index, reduction, grad_scale)
+        return forward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)["loss"].reshape(())
     return LinearCrossEntropyFunction.apply(hidden, weight, labels, ignore_index, reduction)
 
 

@@ -65,12 +65,14 @@ def main():
             F.profile_enable(False)
             for k in cfg:
                 del os.environ[k]
-            res[i].append((e0.elapsed_time(e1) / a.steps, {k: v[0] / a.steps for k, v in prof.items() if v[1]}))
+            res[i].append((e0.elapsed_time(e1) / a.steps, {k: v[0] / a.steps for k, v in prof.items() if v[1]},
+                           {k: v[2] for k, v in prof.items() if v[1] and v[2]}))
     base = statistics.median(r[0] for r in res[0])
     for c, rs in zip(a.configs, res):
         ms = statistics.median(r[0] for r in rs)
         per = {k: round(statistics.median(r[1][k] for r in rs), 2) for k in rs[0][1]}
-        print(f"{ms:8.2f} ms ({(base / ms - 1) * 100:+5.1f}%) [{c or 'default'}] {per}", flush=True)
+        mhz = {k: round(statistics.median(r[2][k] for r in rs)) for k in rs[0][2]}
+        print(f"{ms:8.2f} ms ({(base / ms - 1) * 100:+5.1f}%) [{c or 'default'}] {per} MHz {mhz}", flush=True)
 
 
 if __name__ == "__main__":

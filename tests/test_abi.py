@@ -38,8 +38,8 @@ def test_exports_every_header_symbol(L):
 
 
 def test_version_and_status_strings(L):
-    assert L.lib.lce_abi_version() == L.ABI_VERSION == 2
-    for code in range(11):
+    assert L.lib.lce_abi_version() == L.ABI_VERSION == 3
+    for code in range(13):
         s = L.lib.lce_status_string(code)
         assert s and s != b"unknown status"
     assert L.lib.lce_status_string(99) == b"unknown status"
@@ -120,6 +120,31 @@ def test_backward_host_validation(L):
     a3 = list(args)
     a3[8] = vp(0x10001)
     assert L.lib.lce_backward(ctypes.byref(p), None, *a3) == 3
+    # dweight_flags: bf16 cannot accumulate; unknown bits are rejected (LCE_ERR_ARG)
+    for flags in (L.LCE_DW_BF16 | L.LCE_DW_ACCUMULATE, 4, -1):
+        a4 = list(args)
+        a4[7] = flags
+        assert L.lib.lce_backward(ctypes.byref(p), None, *a4) == 11, flags
+
+
+def test_fused_and_kd_reject_bf16_dweight(L):
+    """The fused / KD paths sum dW over row chunks in fp32: LCE_DW_BF16 -> LCE_ERR_ARG
+    (checked before anything else touches the arguments)."""
+    vp = ctypes.c_void_p
+    p = prob(L, 256, 64, 1000)
+    x = [vp(0x20000 + 0x100 * i) for i in range(12)]
+    assert L.lib.lce_forward_backward(ctypes.byref(p), None, *x[:10], L.LCE_DW_BF16, vp(0x10000), 1 << 30,
+                                      None) == 11
+    assert L.lib.lce_kd_forward_backward(ctypes.byref(p), None, 64, *x[:11], L.LCE_DW_BF16, vp(0x10000), 1 << 30,
+                                         None) == 11
+
+
+def test_expect_grad_and_comm_check_arguments(L):
+    vp = ctypes.c_void_p
+    assert L.lib.lce_expect_grad(None, 1.0, vp(0x10000), None) == 1
+    assert L.lib.lce_expect_grad(vp(0x20000), 1.0, None, None) == 1
+    assert L.lib.lce_expect_grad(vp(0x20000), 1.0, vp(0x10008), None) == 3
+    assert L.lib.lce_comm_check(None) == 0
 
 
 def test_comm_arguments(L):
@@ -148,3 +173,35 @@ def test_product_path_has_no_oracle_or_fallback():
             src = open(os.path.join(pkg, f)).read()
             assert "oracle" not in src.replace("oracle/", "").replace("CPU oracle", ""), f
             assert "torch.nn.functional.cross_entropy" not in src, f
+
+
+def test_binding_does_no_method_arithmetic():
+    """Boundary: the Python layer only marshals arguments.  No
+    arithmetic operator, dtype conversion or torch math is applied to a
+    method output in paper_2605_21442_b200/*.py -- gradient scaling, bf16
+    rounding of dW / dH, loss reductions all happen in liblce.so."""
+    import ast
+
+    pkg = os.path.join(ROOT, "paper_2605_21442_b200")
+    outputs = {"dh", "dw", "dhidden", "dweight", "loss", "lse", "token_loss", "out", "tok"}
+    banned_calls = {"to", "float", "half", "bfloat16", "double", "mul", "mul_", "div", "div_", "add", "add_",
+                    "sum", "mean", "exp", "log", "sub", "sub_", "type"}
+    for f in sorted(os.listdir(pkg)):
+        if not f.endswith(".py"):
+            continue
+        tree = ast.parse(open(os.path.join(pkg, f)).read())
+
+        def base_name(node):
+            while isinstance(node, (ast.Attribute, ast.Subscript)):
+                node = node.value
+            return node.id if isinstance(node, ast.Name) else None
+
+        for node in ast.walk(tree):
+            if isinstance(node, ast.BinOp) and isinstance(node.op, (ast.Mult, ast.Div, ast.Add, ast.Sub, ast.Pow)):
+                for side in (node.left, node.right):
+                    assert base_name(side) not in outputs, (f, node.lineno, ast.unparse(node))
+            if isinstance(node, ast.AugAssign):
+                assert base_name(node.target) not in outputs, (f, node.lineno, ast.unparse(node))
+            if isinstance(node, ast.Call) and isinstance(node.func, ast.Attribute):
+                if node.func.attr in banned_calls:
+                    assert base_name(node.func.value) not in outputs, (f, node.lineno, ast.unparse(node))

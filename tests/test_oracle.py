@@ -17,7 +17,9 @@ from oracle import (
     IGNORE_INDEX,
     combine_shard_stats,
     lce_backward,
+    lce_dweight_rows,
     lce_forward,
+    lce_lse,
     lce_rows,
     shard_stats,
 )
@@ -533,3 +535,56 @@ def test_kd_finite_differences():
                 fp, fm = kd_forward(Hs, ap, Ht, Wt, y)["loss"], kd_forward(Hs, am, Ht, Wt, y)["loss"]
             fd = (fp - fm) / (2 * eps)
             assert abs(fd - grad[idx]) <= 1e-6 * max(1.0, abs(fd)), (name, idx)
+
+
+# ---------------------------------------------------------------- full-size dW helper (sampled vocab rows)
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+def test_dweight_rows_matches_torch_autograd_fp64(reduction):
+    """P10 for lce_dweight_rows / lce_lse (the full-size dW check of the GPU
+    tests): selected rows of dW and every row's lse equal torch's CPU fp64
+    cross_entropy + autograd, including vocab rows nobody is labelled with,
+    rows that are labels, the last row, and a repeated row."""
+    H, W, y = rand_problem(90, 7, 41, 31, ignore_frac=0.2)
+    g = np.linspace(-1.0, 2.0, 90) if reduction == "none" else 0.75
+    J = np.array([0, 40, 40, int(y[y != IGNORE_INDEX][0]), 17, 3])
+    o = lce_dweight_rows(H, W, y, J, reduction=reduction, grad_loss=g)
+    Ht = torch.tensor(H)
+    Wt = torch.tensor(W, requires_grad=True)
+    yt = torch.tensor(y)
+    loss = torch.nn.functional.cross_entropy(Ht @ Wt.T, yt, ignore_index=IGNORE_INDEX, reduction=reduction)
+    if reduction == "none":
+        loss.backward(torch.tensor(g))
+    else:
+        (loss * g).backward()
+    np.testing.assert_allclose(o["dW_rows"], Wt.grad.numpy()[J], rtol=1e-12, atol=1e-14)
+    lse_t = torch.logsumexp(Ht @ torch.tensor(W).T, dim=1).numpy()
+    valid = y != IGNORE_INDEX
+    np.testing.assert_allclose(o["lse"][valid], lse_t[valid], rtol=1e-13, atol=0)
+    assert np.all(o["lse"][~valid] == 0)
+
+
+def test_dweight_rows_finite_differences_and_closed_form():
+    """P4 + P1 for lce_dweight_rows: central differences of the oracle loss
+    in W_jk for the selected rows; with W = 0 (uniform logits) the closed
+    form dW_j = c((1/V) sum_valid h_i - sum_{y_i = j} h_i); block size of the
+    lse pass (host RAM only) changes nothing."""
+    H, W, y = rand_problem(30, 5, 13, 32, ignore_frac=0.2)
+    J = np.array([2, 12, int(y[y != IGNORE_INDEX][1])])
+    o = lce_dweight_rows(H, W, y, J)
+    for a, j in enumerate(J):
+        for k in range(5):
+            eps = 1e-6
+            Wp, Wm = W.copy(), W.copy()
+            Wp[j, k] += eps
+            Wm[j, k] -= eps
+            fd = (lce_forward(H, Wp, y)["loss"] - lce_forward(H, Wm, y)["loss"]) / (2 * eps)
+            assert abs(fd - o["dW_rows"][a, k]) <= 1e-7 * max(1.0, abs(fd))
+    np.testing.assert_array_equal(lce_lse(H, W, y, block=7), lce_lse(H, W, y))
+    Z = np.zeros_like(W)
+    valid = y != IGNORE_INDEX
+    nv = int(valid.sum())
+    oz = lce_dweight_rows(H, Z, y, np.arange(13))
+    for j in range(13):
+        expect = (H[valid].sum(axis=0) / 13 - H[valid & (y == j)].sum(axis=0)) / nv
+        np.testing.assert_allclose(oz["dW_rows"][j], expect, rtol=0, atol=1e-14)
+    assert np.allclose(oz["lse"][valid], math.log(13), rtol=0, atol=1e-14)

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 import torch
 
-from oracle import lce_backward, lce_forward, lce_rows
+from oracle import lce_backward, lce_dweight_rows, lce_forward, lce_lse, lce_rows
 from synth.inputs import CONFIGS, IGNORE, LceInputs, make_config, make_inputs, packed_labels
 
 pytestmark = pytest.mark.gpu
@@ -371,6 +371,35 @@ def test_token_parallel_communicator_one_rank(cuda_lib):
         comm.close()
 
 
+def test_token_parallel_bad_label_status_and_comm_check(cuda_lib):
+    """Token parallelism: the bad-label flag is all-reduced and raised into the
+    status word of every rank (tp_scale_kernel), so every rank's
+    check_device_status reports LCE_ERR_LABEL_RANGE and every loss is NaN
+    (one rank here; tests/test_multi_gpu.py covers two).  lce_comm_check polls
+    NCCL's asynchronous error state (clean here)."""
+    import paper_2605_21442_b200 as F
+
+    comm = F.Comm.single("token")
+    try:
+        inp = small(300, 64, 1000, seed=25)
+        y = inp.labels.clone()
+        y[7] = 5000
+        for fused in (False, True):
+            ws = F.Workspace()
+            if fused:
+                out = F.forward_backward(inp.hidden, inp.weight, y, comm=comm, workspace=ws)
+            else:
+                out = F.forward(inp.hidden, inp.weight, y, comm=comm, workspace=ws)
+            torch.cuda.synchronize()
+            assert math.isnan(out["loss"].item())
+            with pytest.raises(F.LceError) as e:
+                F.check_device_status(ws)
+            assert e.value.code == 6
+        comm.check()
+    finally:
+        comm.close()
+
+
 @pytest.mark.parametrize("path", ["split", "fused"])
 def test_token_parallel_decomposition(cuda_lib, path):
     """What each token-parallel rank computes, checked on one GPU through the
@@ -529,21 +558,106 @@ def test_none_reduction_per_token_logprobs(cuda_lib, variant, N, D, V):
 
 @pytest.mark.parametrize("scale", [1.0, -0.5])
 def test_autograd_fused(cuda_lib, scale):
-    """fused=True: gradients produced in the forward call, scaled by the
-    upstream scalar in backward."""
+    """fused=True: the gradients are produced in the forward call for the
+    upstream gradient stated up front (grad_scale), which the library applies
+    in its epilogues; backward returns them untouched and the device check of
+    the actual upstream gradient stays clean."""
     import paper_2605_21442_b200 as F
 
     inp = small(300, 64, 1000, seed=19)
     h = inp.hidden.clone().requires_grad_(True)
     w = inp.weight.clone().requires_grad_(True)
-    loss = F.linear_cross_entropy(h, w, inp.labels, fused=True)
+    loss = F.linear_cross_entropy(h, w, inp.labels, fused=True, grad_scale=scale)
     (loss * scale).backward()
+    F.check_device_status()
     H, W, y = np_inputs(inp)
     o = lce_forward(H, W, y)
     b = lce_backward(H, W, y, grad_loss=scale)
     assert abs(loss.item() - o["loss"]) <= LOSS_TOL * abs(o["loss"])
     assert fro_rel(h.grad.float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
     assert fro_rel(w.grad.float().cpu().double().numpy(), b["dW"]) <= 2e-2
+
+
+def test_autograd_fused_upstream_mismatch_is_reported(cuda_lib):
+    """An upstream gradient other than the stated grad_scale is never silently
+    rescaled: lce_expect_grad flags it on the device and check_device_status
+    raises LCE_ERR_UPSTREAM; the next call clears the status."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(300, 64, 1000, seed=21)
+    h = inp.hidden.clone().requires_grad_(True)
+    w = inp.weight.clone().requires_grad_(True)
+    loss = F.linear_cross_entropy(h, w, inp.labels, fused=True)
+    (loss * 0.5).backward()
+    with pytest.raises(F.LceError) as e:
+        F.check_device_status()
+    assert e.value.code == 12
+    loss = F.linear_cross_entropy(h, w, inp.labels, fused=True)
+    loss.backward()
+    F.check_device_status()
+
+
+def test_fused_without_grad_runs_forward_only(cuda_lib):
+    """No gradient wanted (torch.no_grad or no input requiring grad): the fused
+    entry runs lce_forward only -- no dH / dW GEMMs, no fp32 dW buffer."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(300, 64, 1000, seed=22)
+    ref = F.linear_cross_entropy(inp.hidden, inp.weight, inp.labels).item()
+    torch.cuda.synchronize()
+    for ctx in (torch.no_grad(), torch.enable_grad()):
+        with ctx:
+            n0 = F.launch_count()
+            loss = F.linear_cross_entropy(inp.hidden, inp.weight, inp.labels, fused=True)
+            torch.cuda.synchronize()
+            assert F.launch_count() - n0 <= 4  # prep, gather, forward GEMM, combine
+            assert loss.item() == ref
+
+
+def test_native_bf16_dweight(cuda_lib):
+    """LCE_DW_BF16: the library rounds the fp32 dW accumulator to bf16 itself
+    (RNE); equal to the bf16 rounding of its own fp32 dW up to one ulp of
+    summation-order difference, and within the gradient bar of the oracle."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(700, 256, 5000, seed=23)
+    out = F.forward(inp.hidden, inp.weight, inp.labels)
+    _, dw32 = F.backward(inp.hidden, inp.weight, inp.labels, out["lse"])
+    _, dw16 = F.backward(inp.hidden, inp.weight, inp.labels, out["lse"], dweight_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    assert dw16.dtype == torch.bfloat16
+    assert torch.equal(dw16, dw32.to(torch.bfloat16))  # same GEMM, same order: exactly RNE(fp32)
+    b = lce_backward(*np_inputs(inp))
+    assert fro_rel(dw16.float().cpu().double().numpy(), b["dW"]) <= GRAD_TOL
+    with pytest.raises(F.LceError):
+        F.backward(inp.hidden, inp.weight, inp.labels, out["lse"], dweight_dtype=torch.bfloat16,
+                   accumulate_dweight=True)
+
+
+def test_binding_rejects_mismatched_shapes(cuda_lib):
+    """Shapes the C ABI would trust are validated in the binding (ValueError /
+    TypeError before any launch)."""
+    import paper_2605_21442_b200 as F
+
+    inp = small(64, 64, 300, seed=24)
+    h, w, y = inp.hidden, inp.weight, inp.labels
+    with pytest.raises(ValueError):
+        F.forward(h, w[:, :56].contiguous(), y)          # D mismatch
+    with pytest.raises(ValueError):
+        F.forward(h, w, y[:63].contiguous())             # labels length
+    out = F.forward(h, w, y)
+    with pytest.raises(TypeError):
+        F.backward(h, w, y, out["lse"].double())         # lse dtype
+    with pytest.raises(ValueError):
+        F.backward(h, w, y, out["lse"][:10].contiguous())  # lse length
+    with pytest.raises(ValueError):
+        F.backward(h, w, y, out["lse"], dweight=torch.empty(299, 64, device="cuda"))
+    with pytest.raises(ValueError):
+        F.backward(h, w, y, out["lse"], grad_loss=torch.ones(2, device="cuda"))
+    with pytest.raises(ValueError):
+        F.forward_backward(h, w, y, dhidden=torch.empty(64, 56, dtype=torch.bfloat16, device="cuda"))
+    with pytest.raises(ValueError):
+        F.kd_forward_backward(h, w, h, w[:200].contiguous(), y)
 
 
 def test_autograd_none_reduction(cuda_lib):
@@ -696,9 +810,10 @@ def test_vocab_shard_full_size_p8_rank(cuda_lib):
     """The per-rank workload of the 8-GPU vocab-parallel 8B run on one GPU:
     rank 2's shard of W (V_l = 16,032 rows, not a tile multiple) at N = 16,384,
     D = 4,096 through the fused path on a one-rank communicator, so the 8,192-row
-    chunks take the wide dH / dW tiles over a ragged vocab extent.  lse / token
-    loss of 256 sampled rows and the full dW shard against the oracle's shard
-    statistics (evaluated in row blocks)."""
+    chunks take the wide dH / dW tiles over a ragged vocab extent.  Every row's
+    lse / token loss and the full dW shard against the oracle's shard
+    statistics, with the shard lse the ORACLE computes for every row
+    (shard_stats in row blocks): no GPU output enters the oracle."""
     import paper_2605_21442_b200 as F
     from oracle import shard_backward, shard_stats
 
@@ -717,18 +832,20 @@ def test_vocab_shard_full_size_p8_rank(cuda_lib):
     H = inp.hidden.float().cpu().numpy()
     Wn = Wsh.float().cpu().numpy()
     y = inp.labels.cpu().numpy()
-    lse_gpu = out["lse"].cpu().double().numpy()
-    rows = np.random.default_rng(5).choice(N, 256, replace=False)
-    st = shard_stats(H[rows], Wn, y[rows], v0, V)
-    lse_sh = st["m"] + np.log(st["s"])
-    assert np.abs(lse_gpu[rows] - lse_sh).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
-    tok = out["token_loss"].cpu().double().numpy()[rows]
-    assert np.abs(tok - (lse_sh - st["z_target"])).max() <= LSE_TOL * max(1, np.abs(lse_sh).max())
-    # the rank's dW rows, with the GPU's (shard-local) lse as the oracle's lse input
+    lse_sh = np.zeros(N)
+    tok_sh = np.zeros(N)
+    for a in range(0, N, 2048):
+        st = shard_stats(H[a:a + 2048], Wn, y[a:a + 2048], v0, V)
+        v = st["valid"]
+        lse_sh[a:a + 2048][v] = st["m"][v] + np.log(st["s"][v])
+        tok_sh[a:a + 2048][v] = lse_sh[a:a + 2048][v] - st["z_target"][v]
+    bound = LSE_TOL * max(1, np.abs(lse_sh).max())
+    assert np.abs(out["lse"].cpu().double().numpy() - lse_sh).max() <= bound
+    assert np.abs(out["token_loss"].cpu().double().numpy() - tok_sh).max() <= bound
     nv = int((y != IGNORE).sum())
     dW = np.zeros((vl, D))
     for a in range(0, N, 2048):
-        dW += shard_backward(H[a:a + 2048], Wn, y[a:a + 2048], v0, lse_gpu[a:a + 2048], 1.0 / nv)["dW_shard"]
+        dW += shard_backward(H[a:a + 2048], Wn, y[a:a + 2048], v0, lse_sh[a:a + 2048], 1.0 / nv)["dW_shard"]
     assert fro_rel(out["dweight"].cpu().double().numpy(), dW) <= GRAD_TOL
 
 
@@ -995,3 +1112,61 @@ def test_full_size_sampled_rows_and_invariants(cuda_lib, name, path):
     assert np.abs(tok.cpu().numpy()[rows] - o["token_loss"]).max() <= LSE_TOL * max(1, np.abs(o["lse"]).max())
     dh_rows = dH[torch.from_numpy(rows).cuda()].float().cpu().double().numpy()
     assert fro_rel(dh_rows, o["dH"]) <= GRAD_TOL
+
+
+# oracle lse of every row of a full-size config (fp64, the oracle's own; shared by both paths)
+_ORACLE_FULL = {}
+
+
+def _oracle_full(name, inp):
+    if name not in _ORACLE_FULL:
+        H = inp.hidden.float().cpu().numpy()
+        W = inp.weight.float().cpu().numpy()
+        y = inp.labels.cpu().numpy()
+        _ORACLE_FULL.clear()  # one config's host copies at a time
+        _ORACLE_FULL[name] = (H, W, y, lce_lse(H, W, y))
+    return _ORACLE_FULL[name]
+
+
+@pytest.mark.parametrize("name,path", [(n, p) for n in ("llama1b", "llama8b", "qwen7b", "llama70b")
+                                       for p in ("fused", "split")])
+def test_full_size_dweight_rows_and_every_lse(cuda_lib, name, path):
+    """Full size, in the bench's launch configuration, independent of the GPU:
+    the oracle computes its own lse for EVERY valid row (lce_lse, fp64, 2 N_v V D
+    flops on the host) and from it the loss, every row's lse / token loss, and
+    sampled rows of dW (lce_dweight_rows: dW_j = sum_i c (p_ij - [y_i = j]) h_i):
+    256 random vocab rows, the whole last 256-row vocab tile (the ragged end of
+    a 512-row wide dW tile at V = 128,256) and the labels of 64 sampled tokens.
+    No oracle input comes from a GPU output."""
+    import paper_2605_21442_b200 as F
+
+    inp = make_config(name, device="cuda")
+    if path == "fused":
+        out = F.forward_backward(inp.hidden, inp.weight, inp.labels, with_token_loss=True)
+        dW = out["dweight"]
+    else:
+        out = F.forward(inp.hidden, inp.weight, inp.labels, with_token_loss=True)
+        _, dW = F.backward(inp.hidden, inp.weight, inp.labels, out["lse"])
+    torch.cuda.synchronize()
+    H, W, y, lse_o = _oracle_full(name, inp)
+    V = W.shape[0]
+    valid = y != IGNORE
+    nv = int(valid.sum())
+    rows = np.flatnonzero(valid)
+    zt = np.einsum("ij,ij->i", H[rows].astype(np.float64), W[y[rows]].astype(np.float64))
+    tok_o = np.zeros(len(y))
+    tok_o[rows] = lse_o[rows] - zt
+    loss_o = tok_o.sum() / nv
+    assert abs(out["loss"].item() - loss_o) <= LOSS_TOL * abs(loss_o), (out["loss"].item(), loss_o)
+    bound = LSE_TOL * max(1.0, np.abs(lse_o).max())
+    assert np.abs(out["lse"].cpu().double().numpy() - lse_o).max() <= bound
+    assert np.abs(out["token_loss"].cpu().double().numpy() - tok_o).max() <= bound
+    rng = np.random.default_rng(7)
+    J = np.unique(np.concatenate([rng.choice(V, 256, replace=False), np.arange(V - 256, V),
+                                  y[rng.choice(rows, 64, replace=False)]]))
+    o = lce_dweight_rows(H, W, y, J, lse=lse_o)
+    got = dW[torch.from_numpy(J).cuda()].cpu().double().numpy()
+    assert fro_rel(got, o["dW_rows"]) <= GRAD_TOL, fro_rel(got, o["dW_rows"])
+    # the rows that are labels carry the -h_i onehot term: check them on their own too
+    lab = np.isin(J, y[rows])
+    assert fro_rel(got[lab], o["dW_rows"][lab]) <= GRAD_TOL
