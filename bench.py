@@ -2,6 +2,9 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config llama8b] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (vocab-parallel, NCCL)
+    python bench.py --gpus N ...   (N > 1 without torchrun: re-launches itself
+                                    under torch.distributed.run with N ranks)
+    python bench.py --sweep llama70b   (1/2/4/8-GPU strong-scaling sweep, t1 / (P tP))
 
 A step is one pass of the whole hot path: lce_forward +
 lce_backward on one synthetic batch already resident in HBM.  value =
@@ -15,6 +18,7 @@ has) on a bounded row sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import functools
 import json
 import os
 import statistics
@@ -87,6 +91,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": smax, "reasons": reasons, "samples": len(rows)}
 
 
+@functools.lru_cache(maxsize=2)
 def oracle_sample(cfg_name: str, n_rows: int, seed: int = 0):
     """Rows of the same workload for the CPU oracle (exact bf16 values)."""
     from synth.inputs import make_inputs, make_labels
@@ -116,51 +121,104 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
 
 
-def time_oracle(cfg_name: str, target_s: float = 12.0):
-    """Oracle fwd+bwd on a bounded row sample; returns (tokens/s, rows, seconds)."""
-    # calibrate on 128 rows (all oracle costs are linear in the row count), then
-    # size the sample for ~target_s seconds of fp64 work
-    H, W, y = oracle_sample(cfg_name, 128)
+def cpu_info():
+    """CPU model and the BLAS behind numpy (the oracle's dgemm)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        for i in threadpool_info():
+            if i.get("user_api") == "blas":
+                blas = f"{i.get('internal_api')} {i.get('version')} ({i.get('threading_layer', '')})".strip()
+                break
+    except Exception:
+        pass
+    return model, blas
+
+
+def oracle_call(cfg_name: str, n: int):
+    """One oracle fwd+bwd on n rows of the workload: (non-ignored rows, seconds)."""
+    H, W, y = oracle_sample(cfg_name, n)
     t0 = time.perf_counter()
-    run_oracle_step(H, W, y)
-    t128 = time.perf_counter() - t0
-    n = int(max(16, min(CONFIGS[cfg_name]["N"], 128 * target_s / max(t128, 1e-3))))
-    H3, W3, y3 = oracle_sample(cfg_name, n)
+    nv = run_oracle_step(H, W, y)
+    return nv, time.perf_counter() - t0
+
+
+def oracle_rows_for(cfg_name: str, seconds: float) -> int:
+    """Rows whose row-proportional oracle work (8 V D fp64 flops per valid row:
+    z in the forward, z, G W and G^T H in the backward) takes ~`seconds` at
+    this host's measured dgemm rate."""
+    c = CONFIGS[cfg_name]
+    a = np.random.default_rng(0).standard_normal((256, 4096))
+    b = np.random.default_rng(1).standard_normal((4096, 4096))
+    a @ b
     t0 = time.perf_counter()
-    nv = run_oracle_step(H3, W3, y3)
-    dt = time.perf_counter() - t0
-    return nv / dt, n, nv, dt
+    for _ in range(3):
+        a @ b
+    rate = 3 * 2 * 256 * 4096 * 4096 / (time.perf_counter() - t0)
+    per_row = 8.0 * c["V"] * c["D"] / rate
+    return int(max(32, min(c["N"] // 2, seconds / per_row)))
+
+
+def marginal_rate(samples):
+    """samples: [(n_rows, nv, seconds)] at two sizes.  The oracle's cost is
+    a + b nv (a: per-call work independent of the row count, e.g. widening W
+    to fp64 in both the forward and the backward); the per-token rate is the
+    marginal 1 / b, so it does not depend on the sample size."""
+    sizes = sorted({n for n, _, _ in samples})
+    lo = [x for x in samples if x[0] == sizes[0]]
+    hi = [x for x in samples if x[0] == sizes[-1]]
+    nv1, t1 = statistics.mean(x[1] for x in lo), statistics.mean(x[2] for x in lo)
+    nv2, t2 = statistics.mean(x[1] for x in hi), statistics.mean(x[2] for x in hi)
+    return (nv2 - nv1) / max(t2 - t1, 1e-9), nv1, t1, nv2, t2
+
+
+def time_oracle(cfg_name: str, target_s: float = 24.0):
+    """Oracle fwd+bwd per-token rate on two bounded row samples (n, 2n)."""
+    n = oracle_rows_for(cfg_name, target_s / 3)
+    samples = [(m, *oracle_call(cfg_name, m)) for m in (n, 2 * n)]
+    rate, nv1, t1, nv2, t2 = marginal_rate(samples)
+    return rate, n, nv1, t1, nv2, t2
+
+
+def cpu_record(rate, n, nv1, t1, nv2, t2, c, calls=2):
+    model, blas = cpu_info()
+    return {"value": rate, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+            "sample": (f"{n} and {2 * n} of {c['N']} rows ({nv1:.0f} / {nv2:.0f} valid), full D={c['D']}, V={c['V']}: "
+                       f"{calls} fp64 fwd+bwd calls, mean {t1:.1f} s / {t2:.1f} s per size; value = marginal per-token "
+                       f"rate (nv2 - nv1) / (t2 - t1), independent of the oracle's per-call fixed cost"),
+            "cpu_model": model, "blas": blas}
 
 
 def reference_arm(args, rank):
     if rank != 0:
         return
     c = CONFIGS[args.config]
-    # each step is a bounded row sample sized so the whole run stays ~1-2 minutes
-    target = min(8.0, max(1.0, 60.0 / max(1, args.steps + min(args.warmup, 1))))
-    H, W, y = oracle_sample(args.config, 128)
-    t0 = time.perf_counter()
-    run_oracle_step(H, W, y)
-    t128 = time.perf_counter() - t0
-    n = int(max(16, min(c["N"], 128 * target / max(t128, 1e-3))))
-    H, W, y = oracle_sample(args.config, n)
+    # steps alternate bounded row samples of n and 2n rows, each ~3-6 s of fp64
+    # work, so the whole run stays within a few minutes; value = marginal rate
+    steps = max(2, args.steps)
+    n = oracle_rows_for(args.config, min(6.0, max(1.0, 90.0 / steps)) / 2)
     for _ in range(min(args.warmup, 1)):
-        run_oracle_step(H, W, y)
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        nv = run_oracle_step(H, W, y)
-        times.append(time.perf_counter() - t0)
-    t = sum(times) / len(times)
-    v = nv / t
-    cores = cpu_threads()
+        oracle_call(args.config, n)
+    samples = []
+    for i in range(steps):
+        m = n * (1 + i % 2)
+        samples.append((m, *oracle_call(args.config, m)))
+    v, nv1, t1, nv2, t2 = marginal_rate(samples)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "steps": steps, "warmup": args.warmup, "ms_per_step": statistics.mean(x[2] for x in samples) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_name(args.config), "N": c["N"], "D": c["D"], "V": c["V"]},
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{n} of {c['N']} rows ({nv} valid), full D={c['D']}, V={c['V']}, fwd+bwd fp64 per step"},
+        "cpu_baseline": cpu_record(v, n, nv1, t1, nv2, t2, c, calls=steps),
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -174,6 +232,97 @@ def workload_name(cfg):
     return f"{tag}: N={c['N']} D={c['D']} V={c['V']}"
 
 
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torch.distributed launcher: re-run this script
+    under torch.distributed.run with N ranks (one process per GPU, rendezvous
+    on 127.0.0.1) and NCCL's INIT log, so the run really has N ranks.  Fails
+    loudly when the box has fewer than N GPUs."""
+    import socket
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}"}), flush=True)
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) visible\n")
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def sweep(args) -> int:
+    """Strong-scaling sweep of one workload over 1/2/4/8 GPUs (vocab-parallel,
+    fixed N): one bench line per P, then efficiency t1 / (P tP).  P larger
+    than the visible GPU count is reported as skipped, never faked."""
+    have = torch.cuda.device_count()
+    res = {}
+    for P in (1, 2, 4, 8):
+        if P > have:
+            res[P] = {"skipped": f"{have} GPU(s) visible"}
+            continue
+        cmd = [sys.executable, os.path.abspath(__file__), "--gpus", str(P), "--config", args.config,
+               "--steps", str(args.steps), "--warmup", str(args.warmup), "--no-cpu-baseline", "--no-e2e",
+               "--no-split", "--path", args.path]
+        outp = subprocess.run(cmd, capture_output=True, text=True).stdout.strip().splitlines()
+        line = next((json.loads(x) for x in reversed(outp) if x.startswith("{")), None)
+        res[P] = {"ms_per_step": line["ms_per_step"], "value": line["value"]} if line and "value" in line else \
+            {"error": "no bench line"}
+    t1 = res[1].get("ms_per_step")
+    for P, r in res.items():
+        if t1 and "ms_per_step" in r:
+            r["efficiency"] = t1 / (P * r["ms_per_step"])
+    print(json.dumps({"sweep": args.config, "path": args.path, "scaling": "strong", "per_gpus": res}), flush=True)
+    return 0
+
+
+def gemm_flops_of(nv_rank, vl, D, fused):
+    f = {k: 2.0 * nv_rank * vl * D for k in ("fwd_gemm", "bwd_dh", "bwd_dw")}
+    if not fused:
+        f["bwd_g"] = 2.0 * nv_rank * vl * D  # the recompute GEMM (fused: an HBM-bound prep kernel)
+    return f
+
+
+def kernel_table(prof, steps, gemm_flops):
+    kernels = {}
+    for k, v in prof.items():
+        if not v[1]:
+            continue
+        kernels[k] = {"ms_per_step": v[0] / steps, "launches_per_step": v[1] / steps}
+        if v[2]:  # GEMM classes: SM clock inside the step (in-kernel clock64 / globaltimer probe)
+            kernels[k]["sm_mhz"] = v[2]
+            if k in gemm_flops:
+                tf = gemm_flops[k] / (v[0] / steps / 1e3) / 1e12
+                kernels[k]["tflops"] = tf
+                # tensor-pipe utilisation at the clock the power cap allowed: achieved / (148 SMs x
+                # 8192 dense bf16 flop/clk x that clock)
+                kernels[k]["util_at_clock"] = tf * 1e12 / (SMS * 8192 * v[2] * 1e6)
+    return kernels
+
+
+def roofline_of(prof, steps, gemm_flops, config, fused, sus, src, step_ms_total):
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom][:2]
+    if dom not in gemm_flops or not dom_n:
+        return None
+    per_launch_flops = gemm_flops[dom] * steps / dom_n
+    achieved = per_launch_flops / (dom_ms / dom_n / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(config + ("_fused" if fused else ""), {}).get(dom)
+    mhz = prof[dom][2]
+    return {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s", "frac": achieved / sus,
+            "sm_mhz": mhz, "util_at_clock": (achieved * 1e12 / (SMS * 8192 * mhz * 1e6)) if mhz else None,
+            "traffic": traffic, "kernel": dom, "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "flops_per_launch": per_launch_flops,
+            "share_of_step": (dom_ms / step_ms_total) if step_ms_total else None}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -183,15 +332,19 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-split", action="store_true", help="skip the recompute-path sub-record")
+    ap.add_argument("--sweep", metavar="CONFIG", default=None,
+                    help="strong-scaling sweep of CONFIG over 1/2/4/8 GPUs (efficiency t1 / (P tP))")
     ap.add_argument("--chunk-budget", type=int, default=0,
-                    help="chunk_budget_bytes (fused: bf16 q/G chunk bytes, default 2 GiB; split: G chunk, 512 MiB)")
+                    help="chunk_budget_bytes (fused: bf16 q/G chunk bytes, default 2 GiB; split: G chunk)")
     ap.add_argument("--parallel", default="vocab", choices=["vocab", "token"],
                     help="N>1: vocab = W sharded by rows, identical batch on every rank (P:180 loss parallel, the "
                          "benchmarked mode); token = W replicated, the batch's rows split over ranks, N_v and the loss "
                          "exchanged by the library and dW all-reduced (the data-parallel gradient reduction)")
     ap.add_argument("--path", default="auto", choices=["auto", "fused", "split"],
                     help="fused = lce_forward_backward (no logit recompute, 6 N_v V D flops); split = "
-                         "lce_forward + lce_backward (recompute from lse, 8 N_v V D flops); auto = fused")
+                         "lce_forward + lce_backward (recompute from lse, 8 N_v V D flops); auto = fused, with "
+                         "the split path as a sub-record")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -200,6 +353,14 @@ def main():
 
     if args.impl == "reference":
         return reference_arm(args, rank)
+    if args.sweep:
+        args.config = args.sweep
+        return sweep(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU\n")
+        return 2
 
     import paper_2605_21442_b200 as F
     from paper_2605_21442_b200.dist import max_over_ranks
@@ -226,6 +387,7 @@ def main():
         r0, nr = F.shard_range(N, world, rank)
         H, y = H[r0:r0 + nr].clone(), y[r0:r0 + nr].clone()
         N = nr
+    nv_rank = nv if not token else int((y != IGNORE).sum().item())  # rows this rank projects
     ws = F.Workspace()
     stream = torch.cuda.current_stream()
     out = {
@@ -234,10 +396,9 @@ def main():
     }
     dH = torch.empty_like(H)
     dW = torch.empty(vl, D, dtype=torch.float32, device=dev)
+    fused_head = args.path in ("fused", "auto")
 
-    fused = args.path in ("fused", "auto")
-
-    def run_path(Hx, Wx, yx):
+    def run_path(Hx, Wx, yx, fused):
         if fused:  # lce_forward_backward: logits kept per row chunk, 6 N_v V D flops
             F.forward_backward(Hx, Wx, yx, dhidden=dH, dweight=dW, workspace=ws, out=out,
                                chunk_budget_bytes=args.chunk_budget, comm=comm, vocab_start=vstart, vocab_total=V)
@@ -247,77 +408,79 @@ def main():
             F.backward(Hx, Wx, yx, out["lse"], comm=comm, vocab_start=vstart, vocab_total=V, dhidden=dH,
                        dweight=dW, workspace=ws, chunk_budget_bytes=args.chunk_budget)
 
-    def step():
-        run_path(H, W, y)
+    def step(fused):
+        run_path(H, W, y, fused)
         if token:  # the data-parallel gradient reduction of the replicated head
             dist.all_reduce(dW)
 
+    def timed(fused, steps, profile=False, clocks=False):
+        """W warm-up steps, then `steps` steps bracketed by barrier + synchronize,
+        one CUDA event pair per step on the launching stream.  Returns
+        (total ms (max over ranks), per-step ms list, launches, profile, clocks)."""
+        for _ in range(args.warmup):
+            step(fused)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        clk = ClockSampler(local) if clocks else None
+        if clk:
+            clk.start()
+        if profile:
+            F.profile_enable(True)
+        l0 = F.launch_count()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for i in range(steps):
+            step(fused)
+            ev[i + 1].record(stream)
+        torch.cuda.synchronize()
+        launches = F.launch_count() - l0
+        prof = None
+        if profile:
+            prof = F.profile_read()
+            F.profile_enable(False)
+        clk_rec = clk.stop() if clk else None
+        per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+        total = ev[0].elapsed_time(ev[steps])
+        if dist:  # the job's step time is the slowest rank's (device time, max over ranks)
+            total = max_over_ranks(total, device=dev)
+            per = [max_over_ranks(x, device=dev) for x in per]
+            dist.barrier()
+        return total, per, launches, prof, clk_rec
+
     torch.cuda.reset_peak_memory_stats(dev)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    F.profile_enable(True)
-    l0 = F.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    launches = F.launch_count() - l0
-    prof = F.profile_read()
-    F.profile_enable(False)
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    if dist:  # the job's step time is the slowest rank's (device time, max over ranks)
-        ms = max_over_ranks(ms, device=dev)
-        dist.barrier()
+    # headline: profiler off; clocks sampled during the timed region
+    ms, per, launches, _, clk = timed(fused_head, args.steps, clocks=True)
     peak_hbm = torch.cuda.max_memory_allocated(dev)
     ms_step = ms / args.steps
     value = nv * args.steps / (ms / 1e3)
     sus, burst, hbm, src = peaks()
-    flops_step = (6.0 if fused else 8.0) * nv * V * D  # executed tensor-core flops per step
+    flops_step = (6.0 if fused_head else 8.0) * nv * V * D  # executed tensor-core flops per step
     tensor_frac = flops_step / (ms_step / 1e3) / (sus * 1e12 * world)
+    # per-kernel profile in a separate pass (CUDA events around every launch)
+    pms, _, _, prof, _ = timed(fused_head, args.steps, profile=True)
+    gflops = gemm_flops_of(nv_rank, vl, D, fused_head)
+    kernels = kernel_table(prof, args.steps, gflops)
+    roof = roofline_of(prof, args.steps, gflops, args.config, fused_head, sus, src, pms if world == 1 else None)
 
-    # dominant kernel (by device time inside the timed region, on the launching stream)
-    nv_rank = nv if not token else int((y != IGNORE).sum().item())  # rows this rank projects
-    gemm_flops = {k: 2.0 * nv_rank * vl * D for k in ("fwd_gemm", "bwd_dh", "bwd_dw")}
-    if not fused:
-        gemm_flops["bwd_g"] = 2.0 * nv_rank * vl * D  # the recompute GEMM (fused: an HBM-bound fix-up kernel)
-    dom = max(prof, key=lambda k: prof[k][0])
-    dom_ms, dom_n = prof[dom][:2]
-    kernels = {}
-    for k, v in prof.items():
-        if not v[1]:
-            continue
-        kernels[k] = {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
-        if v[2]:  # GEMM classes: SM clock inside the step (in-kernel clock64 / globaltimer probe)
-            kernels[k]["sm_mhz"] = v[2]
-            if k in gemm_flops:
-                tf = gemm_flops[k] / (v[0] / args.steps / 1e3) / 1e12
-                kernels[k]["tflops"] = tf
-                # tensor-pipe utilisation at the clock the power cap allowed: achieved / (148 SMs x
-                # 8192 dense bf16 flop/clk x that clock)
-                kernels[k]["util_at_clock"] = tf * 1e12 / (SMS * 8192 * v[2] * 1e6)
-    roof = None
-    if dom in gemm_flops and dom_n:
-        per_launch_flops = gemm_flops[dom] * args.steps / dom_n
-        achieved = per_launch_flops / (dom_ms / dom_n / 1e3) / 1e12
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            traffic = json.load(open(tp)).get(args.config + ("_fused" if fused else ""), {}).get(dom)
-        mhz = prof[dom][2]
-        roof = {"bound": "tensor", "achieved": achieved, "peak": sus, "unit": "TFLOP/s", "frac": achieved / sus,
-                "sm_mhz": mhz, "util_at_clock": (achieved * 1e12 / (SMS * 8192 * mhz * 1e6)) if mhz else None,
-                "traffic": traffic, "kernel": dom, "peak_source": f"{src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
-                "flops_per_launch": per_launch_flops,
-                "share_of_step": dom_ms / ms if world == 1 else None}
+    # the north star's recompute path (lce_forward + lce_backward) as a sub-record
+    split = None
+    if fused_head and not args.no_split:
+        sms_total, sper, slaunch, _, sclk = timed(False, args.steps, clocks=True)
+        spms, _, _, sprof, _ = timed(False, args.steps, profile=True)
+        sg = gemm_flops_of(nv_rank, vl, D, False)
+        s_step = sms_total / args.steps
+        split = {"path": "lce_forward + lce_backward (backward recomputes the logit tiles from the saved lse)",
+                 "value": nv * args.steps / (sms_total / 1e3), "unit": "tokens/s", "ms_per_step": s_step,
+                 "ms_per_step_median": statistics.median(sper), "ms_per_step_min": min(sper),
+                 "ms_per_step_max": max(sper), "flops_per_step": 8.0 * nv * V * D,
+                 "tensor_frac": 8.0 * nv * V * D / (s_step / 1e3) / (sus * 1e12 * world),
+                 "tensor_frac_note": f"8*N_v*V*D algorithmic flops (SURVEY 8d) / (time x {src} sustained bf16 peak x GPUs)",
+                 "roofline": roofline_of(sprof, args.steps, sg, args.config, False, sus, src,
+                                         spms if world == 1 else None),
+                 "kernels": kernel_table(sprof, args.steps, sg), "gpu_launches_per_step": slaunch / args.steps,
+                 "clocks": sclk}
 
     # e2e through the public API with host buffers (pinned): every step copies
     # its H, W, y host->device and reads its loss back, inside the timed region.
@@ -338,8 +501,8 @@ def main():
             k = i % 2
             cstream.wait_event(consumed[k])  # the compute of step i-2 released this buffer set
             with torch.cuda.stream(cstream):
-                for dst, src in zip(bufs[k], (Hh, Wh, yh)):
-                    dst.copy_(src, non_blocking=True)
+                for dst, src_ in zip(bufs[k], (Hh, Wh, yh)):
+                    dst.copy_(src_, non_blocking=True)
             loaded[k].record(cstream)
 
         def e2e_steps(n):
@@ -349,7 +512,9 @@ def main():
                     issue_copy(i + 1)
                 k = i % 2
                 stream.wait_event(loaded[k])
-                run_path(*bufs[k])
+                run_path(*bufs[k], fused_head)
+                if token:
+                    dist.all_reduce(dW)
                 consumed[k].record(stream)
                 lossh[i].copy_(out["loss"][0], non_blocking=True)
 
@@ -373,33 +538,36 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_cpu, n_rows, nv_rows, dt = time_oracle(args.config)
-        cpu = {"value": v_cpu, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
-               "sample": f"{n_rows} of {N} rows ({nv_rows} valid), full D={D}, V={V}, one fp64 fwd+bwd in {dt:.1f}s"}
+        cpu = cpu_record(*time_oracle(args.config), c)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": statistics.median(per),
+            "ms_per_step_min": min(per), "ms_per_step_max": max(per), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": workload_name(args.config), "N": c["N"], "N_valid": nv, "D": D, "V": V,
                        "parallelism": f"{args.parallel}-parallel x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (W alone is %.2f GB > 126 MB); no flush" % (V * D * 2 / 1e9)},
-            "path": "fused lce_forward_backward" if fused else "lce_forward + lce_backward",
+            "path": "fused lce_forward_backward" if fused_head else "lce_forward + lce_backward",
             "flops_per_step": flops_step,
             "tensor_frac": tensor_frac,
-            "tensor_frac_note": f"{'6' if fused else '8'}*N_v*V*D executed flops per step / (time x {src} sustained bf16 peak x GPUs)",
+            "tensor_frac_note": f"{'6' if fused_head else '8'}*N_v*V*D executed flops per step / (time x {src} sustained bf16 peak x GPUs)",
             "peak_hbm_bytes": peak_hbm, "naive_logits_bytes_fp32": c["N"] * V * 4,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
             "clocks": clk, "kernels": kernels,
+            "kernels_note": "per-kernel times from a separate profiled pass (CUDA events around every launch); "
+                            "the headline step time is measured with the profiler off",
+            "split": split,
         }
         print(json.dumps(line), flush=True)
     if comm:
         comm.close()
     if dist:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

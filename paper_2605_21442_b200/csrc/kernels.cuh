@@ -66,9 +66,65 @@ struct EpiLse : EpiBase {
     // kScaledQMax raise *q_flag (the chunk is then redone in the tile-max form)
     const float* q_ref;
     int32_t* q_flag;
+    // scaled-q mode, one TMEM pass (one GPU): the partials are taken relative
+    // to the reference too -- (m, s) = (ref_i, sum_j exp(z_ij - ref_i)) -- so
+    // neither the tile max nor a second pass over the accumulator is needed.
+    // A row with z - ref > kScaledQMax flags its chunk, whose fallback redoes
+    // the forward (tile-max form) and the combine.
+    int32_t one_pass;
   };
   static __device__ __forceinline__ void finish(const Params& p) {
     if ((p.use_zmap || p.store_q) && (threadIdx.x & 31) == 0) tma_store_wait_all();
+  }
+  // One pass over the accumulator: e = exp(z - ref) (masked past n_cols),
+  // summed in fp32 and stored as bf16 q; the target logit picked on the way.
+  template <bool kFull>
+  static __device__ __forceinline__ void one_pass_ref(const Params& p, uint32_t taddr, TileInfo& t, int r, bool valid,
+                                                      int yl) {
+    const float ref = valid ? p.q_ref[p.row_off + r] : 0.f;
+    const float rl = ref * kLog2e;
+    const float lim = ref + kScaledQMax;
+    float s = 0.f, zt = 0.f;
+    bool over = false;
+#pragma unroll 1
+    for (int c2 = 0; c2 < BN / 64; ++c2) {
+      uint32_t w[32];
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float x[32];
+        const int c = 2 * c2 + h;
+        load_chunk(taddr, c, t.zero_acc, x);
+        const int cb = t.n0 + c * 32;
+        if ((yl >> 5) == c) {
+          const int jt = yl & 31;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j == jt) zt = x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const bool in0 = kFull || cb + j < p.n_cols, in1 = kFull || cb + j + 1 < p.n_cols;
+          over |= (in0 && x[j] > lim) || (in1 && x[j + 1] > lim);
+          const float e0 = in0 ? ex2_approx(fmaf(x[j], kLog2e, -rl)) : 0.f;
+          const float e1 = in1 ? ex2_approx(fmaf(x[j + 1], kLog2e, -rl)) : 0.f;
+          a0 += e0;
+          a1 += e1;
+          w[h * 16 + j / 2] = pack_bf16x2(e0, e1);
+        }
+      }
+      s += a0 + a1;
+      uint4 u[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) u[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+      tma_rows(p, t, t.n0 + c2 * 64, u);
+    }
+    if (valid) {
+      p.part_m[t.n_blk * p.ld + r] = ref;
+      p.part_s[t.n_blk * p.ld + r] = s;
+      if (yl >= 0 && yl < BN && t.n0 + yl < p.n_cols) p.zt[p.row_off + r] = zt;
+      if (over) *p.q_flag = 1;
+    }
   }
   // Stage this warp's 32 rows x 128 bytes in the 128B-swizzled tile (16-byte
   // unit v of row l at unit v ^ (l & 7)) and let lane 0 issue the TMA store
@@ -123,6 +179,13 @@ struct EpiLse : EpiBase {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[p.row_off + r] - p.label_off - t.n0) : -1;  // tile-relative target column
+    if (p.one_pass) {
+      if (t.n0 + BN <= p.n_cols)
+        one_pass_ref<true>(p, taddr, t, r, valid, yl);
+      else
+        one_pass_ref<false>(p, taddr, t, r, valid, yl);
+      return;
+    }
     float4* zrow = (p.z && valid) ? reinterpret_cast<float4*>(p.z + static_cast<int64_t>(r) * p.ldz + t.n0) : nullptr;
     float m = -INFINITY, zt = 0.f;
 #pragma unroll 1
@@ -699,8 +762,8 @@ __global__ void expect_grad_kernel(const float* __restrict__ grad, float expecte
 }
 
 // ============================================================ S0 gather
-// Block b: compact row b <- H[idx[b]] (zeros for b in [N_v, ceil128(N_v)) so
-// whole 128-row tiles and 64-row k-blocks read finite zeros), optional lse
+// Block b: compact row b <- H[idx[b]] (zeros for b in [N_v, ceil256(N_v)) so
+// whole 256-row pair tiles and 64-row k-blocks read finite zeros), optional lse
 // gather for the backward, optional zeroing of dhidden row b if token b is
 // excluded (ignored or bad label: its gradient is exactly 0).
 __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict__ H, int64_t D, int N,
@@ -720,7 +783,7 @@ __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict_
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
     if (lse_in && threadIdx.x == 0) lse_c[b] = lse_in[src_row];
     if (grad_in && threadIdx.x == 0) grad_c[b] = grad_in[src_row];
-  } else if (b < ((nv + 127) & ~127)) {
+  } else if (b < ((nv + 255) & ~255)) {  // up to the 256-row pair tile: no stale row enters a GEMM
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
   }
   if (dhidden && b < N) {
@@ -882,7 +945,9 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
                                                            float* __restrict__ lse_out, float* __restrict__ tok_out,
                                                            float* __restrict__ lse_c, float* __restrict__ ltok,
                                                            const float* __restrict__ q_ref = nullptr,
-                                                           int32_t* __restrict__ q_flag = nullptr) {
+                                                           int32_t* __restrict__ q_flag = nullptr,
+                                                           const int32_t* __restrict__ gate = nullptr) {
+  if (gate && *gate == 0) return;  // the fallback's re-combine: empty unless the chunk was flagged
   const int m = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5);  // one warp per row
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= M) return;

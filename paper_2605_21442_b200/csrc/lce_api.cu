@@ -1037,7 +1037,9 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
     EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
     ep.use_map = dw_tma();
     ep.dbg = dbg_epi();
-    ep.prefetch = !(getenv("LCE_DW_PREFETCH") && atoi(getenv("LCE_DW_PREFETCH")) == 0);
+    // L2 prefetch of the old dW rows before the reduce-adds: measured 0.5-1.3%
+    // slower per step (8B / 70B fused), so off unless LCE_DW_PREFETCH=1
+    ep.prefetch = getenv("LCE_DW_PREFETCH") && atoi(getenv("LCE_DW_PREFETCH")) == 1;
     if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
     // runs beside this chunk's dH all-reduce under vocab parallelism
     LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, overlap_sms(comm, sms), s,
@@ -1162,6 +1164,10 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   // (no host sync; under vocab parallelism each rank decides for its own
   // partials).  LCE_FUSED_SCALED=0 selects the fix-up form.
   const bool scaled = !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
+  // one TMEM pass in the forward epilogue (partials relative to the reference;
+  // one GPU or token parallel: under vocab parallelism a rank's fallback could
+  // not redo the cross-rank combine alone).  LCE_FWD_ONEPASS=0: two passes.
+  const bool one_pass = scaled && !comm && !(getenv("LCE_FWD_ONEPASS") && atoi(getenv("LCE_FWD_ONEPASS")) == 0);
   float* qref = reinterpret_cast<float*>(ws + fp.qref);
   float* coef = reinterpret_cast<float*>(ws + fp.coef);
   uint16_t* hs = reinterpret_cast<uint16_t*>(ws + fp.hs);
@@ -1192,6 +1198,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       ep.store_q = 1;
       ep.q_ref = scaled ? qref : nullptr;
       ep.q_flag = scaled ? qflag : nullptr;
+      ep.one_pass = one_pass ? 1 : 0;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
@@ -1241,6 +1248,12 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       ep.store_q = 1;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_BWD_G, t_h_k, t_w_k, d, ep, dev.sms, s)));
+      if (one_pass) {  // the one-pass partials of a flagged chunk may have overflowed: combine again
+        LaunchScope sc(LCE_K_COMBINE, s);
+        combine_rows_kernel<<<cb, 256, 0, s>>>(pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse,
+                                              token_loss, lsec, ltok, nullptr, nullptr, redo_rows);
+        LCE_TRY(last_error());
+      }
     }
     {  // S4 without recompute: G = s_i (softmax - onehot) from the kept q, in place
       // (scaled form: only on the fallback)
