@@ -66,65 +66,9 @@ struct EpiLse : EpiBase {
     // kScaledQMax raise *q_flag (the chunk is then redone in the tile-max form)
     const float* q_ref;
     int32_t* q_flag;
-    // scaled-q mode, one TMEM pass (one GPU): the partials are taken relative
-    // to the reference too -- (m, s) = (ref_i, sum_j exp(z_ij - ref_i)) -- so
-    // neither the tile max nor a second pass over the accumulator is needed.
-    // A row with z - ref > kScaledQMax flags its chunk, whose fallback redoes
-    // the forward (tile-max form) and the combine.
-    int32_t one_pass;
   };
   static __device__ __forceinline__ void finish(const Params& p) {
     if ((p.use_zmap || p.store_q) && (threadIdx.x & 31) == 0) tma_store_wait_all();
-  }
-  // One pass over the accumulator: e = exp(z - ref) (masked past n_cols),
-  // summed in fp32 and stored as bf16 q; the target logit picked on the way.
-  template <bool kFull>
-  static __device__ __forceinline__ void one_pass_ref(const Params& p, uint32_t taddr, TileInfo& t, int r, bool valid,
-                                                      int yl) {
-    const float ref = valid ? p.q_ref[p.row_off + r] : 0.f;
-    const float rl = ref * kLog2e;
-    const float lim = ref + kScaledQMax;
-    float s = 0.f, zt = 0.f;
-    bool over = false;
-#pragma unroll 1
-    for (int c2 = 0; c2 < BN / 64; ++c2) {
-      uint32_t w[32];
-      float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float x[32];
-        const int c = 2 * c2 + h;
-        load_chunk(taddr, c, t.zero_acc, x);
-        const int cb = t.n0 + c * 32;
-        if ((yl >> 5) == c) {
-          const int jt = yl & 31;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j == jt) zt = x[j];
-        }
-#pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const bool in0 = kFull || cb + j < p.n_cols, in1 = kFull || cb + j + 1 < p.n_cols;
-          over |= (in0 && x[j] > lim) || (in1 && x[j + 1] > lim);
-          const float e0 = in0 ? ex2_approx(fmaf(x[j], kLog2e, -rl)) : 0.f;
-          const float e1 = in1 ? ex2_approx(fmaf(x[j + 1], kLog2e, -rl)) : 0.f;
-          a0 += e0;
-          a1 += e1;
-          w[h * 16 + j / 2] = pack_bf16x2(e0, e1);
-        }
-      }
-      s += a0 + a1;
-      uint4 u[8];
-#pragma unroll
-      for (int v = 0; v < 8; ++v) u[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
-      tma_rows(p, t, t.n0 + c2 * 64, u);
-    }
-    if (valid) {
-      p.part_m[t.n_blk * p.ld + r] = ref;
-      p.part_s[t.n_blk * p.ld + r] = s;
-      if (yl >= 0 && yl < BN && t.n0 + yl < p.n_cols) p.zt[p.row_off + r] = zt;
-      if (over) *p.q_flag = 1;
-    }
   }
   // Stage this warp's 32 rows x 128 bytes in the 128B-swizzled tile (16-byte
   // unit v of row l at unit v ^ (l & 7)) and let lane 0 issue the TMA store
@@ -179,13 +123,6 @@ struct EpiLse : EpiBase {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
     const int yl = valid ? (p.yc[p.row_off + r] - p.label_off - t.n0) : -1;  // tile-relative target column
-    if (p.one_pass) {
-      if (t.n0 + BN <= p.n_cols)
-        one_pass_ref<true>(p, taddr, t, r, valid, yl);
-      else
-        one_pass_ref<false>(p, taddr, t, r, valid, yl);
-      return;
-    }
     float4* zrow = (p.z && valid) ? reinterpret_cast<float4*>(p.z + static_cast<int64_t>(r) * p.ldz + t.n0) : nullptr;
     float m = -INFINITY, zt = 0.f;
 #pragma unroll 1
@@ -336,6 +273,12 @@ struct EpiDH : EpiBase {
                            //    finalize pass applies c, rounds and scatters
     alignas(64) CUtensorMap map;  // acc_buf [rows, ld] fp32, 32 x 32 boxes, 128B swizzle
     const float* row_coef;  // scaled-q mode: per chunk-row factor s_i beta_i of the direct path (null: none)
+    // NVLS (vocab-parallel, LCE_NVLS=1): add row r of the (row_coef-scaled)
+    // accumulator into the multicast-mapped fp32 buffer [rows][ld]: the switch
+    // sums every rank's (and every split-K item's) partial into every GPU's
+    // copy -- the dH all-reduce fused into this epilogue
+    float* mc_out;
+    int32_t mc_unicast;  // LCE_NVLS=2 (one-rank emulation): plain red.global.add into a unicast buffer
   };
   // pull the running fp32 sum of this tile's row into L2 while the MMA runs
   static __device__ __forceinline__ void prefetch(const Params& p, const TileInfo& t) {
@@ -350,6 +293,32 @@ struct EpiDH : EpiBase {
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     const int r = t.m0 + t.row;
     const bool valid = r < t.M;
+    if (p.mc_out) {  // NVLS: in-switch reduction straight from registers
+      const float rc = (p.row_coef && valid) ? p.row_coef[r] : 1.f;
+      float* orow = p.mc_out + static_cast<int64_t>(r) * p.ld;
+      uint32_t v[2][32];
+      tmem_ld32(taddr, v[0]);
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        tmem_ld_wait();
+        if (c + 1 < BN / 32) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+        const uint32_t* u = v[c & 1];
+        const int cb = t.n0 + c * 32;
+        if (!valid || t.zero_acc || cb >= t.N) continue;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int col = cb + 4 * q;
+          if (col >= t.N) break;
+          const float a = rc * __uint_as_float(u[4 * q]), b = rc * __uint_as_float(u[4 * q + 1]);
+          const float c2 = rc * __uint_as_float(u[4 * q + 2]), d = rc * __uint_as_float(u[4 * q + 3]);
+          if (p.mc_unicast)
+            red_add_v4(orow + col, a, b, c2, d);
+          else
+            multimem_red_add_v4(orow + col, a, b, c2, d);
+        }
+      }
+      return;
+    }
     if (p.use_map && !p.part) {  // TMA store / reduce-add of the unscaled chunk sum
       const int l = t.row & 31;
 #pragma unroll 1
@@ -756,6 +725,21 @@ __global__ void tp_scale_kernel(Header* hdr, const float* __restrict__ grad_loss
   if (hdr->n_valid > 0 && reduction == 0) hdr->c = nv == 0 ? 0.f : g / static_cast<float>(nv);
 }
 
+// NVLS barrier across the ranks of a multicast buffer: every rank release-adds
+// 1 to the counter in every GPU's copy (through the switch), then waits until
+// its own copy reaches `target` (= barriers so far x ranks).  The fence makes
+// this stream's earlier multimem reductions visible system-wide first.
+__global__ void nvls_barrier_kernel(uint32_t* mc_flag, const uint32_t* uc_flag, uint32_t target, int unicast) {
+  if (threadIdx.x != 0) return;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (unicast)
+    atomicAdd(mc_flag, 1u);
+  else
+    multimem_red_release_add_u32(mc_flag, 1u);
+  while (ld_acquire_sys_u32(uc_flag) < target) {
+  }
+}
+
 // lce_expect_grad: the upstream gradient the fused call assumed vs the actual one.
 __global__ void expect_grad_kernel(const float* __restrict__ grad, float expected, Header* hdr) {
   if (*grad != expected) hdr->status |= kStatusUpstream;
@@ -945,9 +929,7 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const float* __restri
                                                            float* __restrict__ lse_out, float* __restrict__ tok_out,
                                                            float* __restrict__ lse_c, float* __restrict__ ltok,
                                                            const float* __restrict__ q_ref = nullptr,
-                                                           int32_t* __restrict__ q_flag = nullptr,
-                                                           const int32_t* __restrict__ gate = nullptr) {
-  if (gate && *gate == 0) return;  // the fallback's re-combine: empty unless the chunk was flagged
+                                                           int32_t* __restrict__ q_flag = nullptr) {
   const int m = blockIdx.x * kRowsPerCta + (threadIdx.x >> 5);  // one warp per row
   const int M = min(max(hdr->n_valid - row_off, 0), cap);
   if (m >= M) return;

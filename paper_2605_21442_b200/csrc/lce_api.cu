@@ -2,8 +2,11 @@
 // workspace planning, TMA descriptor encoding, launch sequencing, the
 // vocab-parallel NCCL layer and the opt-in kernel profiler.
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -588,6 +591,7 @@ struct NcclApi {
   ncclResult_t (*groupStart)();
   ncclResult_t (*groupEnd)();
   ncclResult_t (*getAsyncError)(ncclComm_t, ncclResult_t*);
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
 };
 
 NcclApi* nccl() {
@@ -606,6 +610,7 @@ NcclApi* nccl() {
     api.groupStart = reinterpret_cast<decltype(api.groupStart)>(dlsym(h, "ncclGroupStart"));
     api.groupEnd = reinterpret_cast<decltype(api.groupEnd)>(dlsym(h, "ncclGroupEnd"));
     api.getAsyncError = reinterpret_cast<decltype(api.getAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+    api.broadcast = reinterpret_cast<decltype(api.broadcast)>(dlsym(h, "ncclBroadcast"));
     api.ok = api.getUniqueId && api.commInitRank && api.commDestroy && api.allReduce;
   });
   return api.ok ? &api : nullptr;
@@ -613,12 +618,29 @@ NcclApi* nccl() {
 
 }  // namespace
 
+// NVLS state of a vocab-parallel communicator (LCE_NVLS=1): one multicast
+// object over every rank's GPU, bound to a local fp32 buffer on each, mapped
+// twice -- the multicast VA (the dH epilogue's multimem.red.add target: the
+// switch adds into every GPU's copy) and the local unicast VA (read back by
+// the cast / scatter).  The last 4 KB hold the NVLS barrier counter.
+struct NvlsBuf {
+  bool ready = false;
+  size_t bytes = 0, size = 0;
+  CUmemGenericAllocationHandle mc = 0, phys = 0;
+  CUdeviceptr uc = 0, mcva = 0;
+  uint32_t barriers = 0;  // barriers issued so far on this buffer
+  int dev = -1;
+  bool unicast = false;   // LCE_NVLS=2 on a one-rank communicator: cudaMalloc'd stand-in
+};
+
 struct lce_comm_s {
   ncclComm_t comm;
   int nranks, rank;
   int mode;  // lce_parallel_t
   cudaStream_t side;          // runs the dH all-reduce concurrently with the last dW GEMM
   cudaEvent_t dh_ready, dh_reduced;
+  NvlsBuf nvls;
+  void* scratch = nullptr;    // 256 B of device memory for the NVLS setup exchange
 };
 
 namespace {
@@ -638,6 +660,262 @@ int overlap_sms(lce_comm_t comm, int sms) {
   return (sms - r) & ~1;
 }
 
+
+// ------------------------------------------------------------------ NVLS (in-switch dH reduction)
+// LCE_NVLS=1 with a vocab-parallel communicator: the dH partials are added into
+// a multicast buffer by the dH GEMM's epilogue (multimem.red.add.v4.f32) instead
+// of an NCCL all-reduce afterwards -- the GEMM and its collective are one
+// kernel, no SMs are held back for NCCL, and the partials never make a second
+// trip through HBM.  Gated on CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED on every
+// rank.  Summation order inside the switch is not fixed, so dH is not bitwise
+// reproducible in this mode (the NCCL path is).
+struct DrvApi {
+  bool ok = false;
+  PFN_cuMulticastCreate mcCreate;
+  PFN_cuMulticastAddDevice mcAdd;
+  PFN_cuMulticastBindMem mcBind;
+  PFN_cuMulticastUnbind mcUnbind;
+  PFN_cuMulticastGetGranularity mcGran;
+  PFN_cuMemCreate memCreate;
+  PFN_cuMemRelease memRelease;
+  PFN_cuMemAddressReserve addrReserve;
+  PFN_cuMemAddressFree addrFree;
+  PFN_cuMemMap memMap;
+  PFN_cuMemUnmap memUnmap;
+  PFN_cuMemSetAccess setAccess;
+  PFN_cuMemExportToShareableHandle exportH;
+  PFN_cuMemImportFromShareableHandle importH;
+  PFN_cuDeviceGet devGet;
+  PFN_cuDeviceGetAttribute devAttr;
+};
+
+DrvApi* drv() {
+  static DrvApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    bool ok = true;
+    auto get = [&](const char* name, auto& fn) {
+      void* ptr = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &ptr, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+        ok = false;
+      fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(ptr);
+    };
+    get("cuMulticastCreate", api.mcCreate);
+    get("cuMulticastAddDevice", api.mcAdd);
+    get("cuMulticastBindMem", api.mcBind);
+    get("cuMulticastUnbind", api.mcUnbind);
+    get("cuMulticastGetGranularity", api.mcGran);
+    get("cuMemCreate", api.memCreate);
+    get("cuMemRelease", api.memRelease);
+    get("cuMemAddressReserve", api.addrReserve);
+    get("cuMemAddressFree", api.addrFree);
+    get("cuMemMap", api.memMap);
+    get("cuMemUnmap", api.memUnmap);
+    get("cuMemSetAccess", api.setAccess);
+    get("cuMemExportToShareableHandle", api.exportH);
+    get("cuMemImportFromShareableHandle", api.importH);
+    get("cuDeviceGet", api.devGet);
+    get("cuDeviceGetAttribute", api.devAttr);
+    api.ok = ok;
+  });
+  return api.ok ? &api : nullptr;
+}
+
+// 1: NVLS; 2: its one-rank emulation (a unicast buffer and plain reductions:
+// the same zero / add / barrier / read-back sequence, for boxes whose driver
+// refuses multicast objects -- tests only)
+int nvls_requested() {
+  const char* e = getenv("LCE_NVLS");
+  const int v = e ? atoi(e) : 0;
+  return (v == 1 || v == 2) ? v : 0;
+}
+
+#define LCE_CU(expr)                                                                           \
+  do {                                                                                         \
+    CUresult r_ = (expr);                                                                      \
+    if (r_ != CUDA_SUCCESS) {                                                                  \
+      if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: %s -> CUresult %d\n", #expr, (int)r_);    \
+      return LCE_ERR_CUDA;                                                                     \
+    }                                                                                          \
+  } while (0)
+
+void nvls_release(lce_comm_t c) {
+  NvlsBuf& b = c->nvls;
+  if (b.unicast) {
+    cudaFree(reinterpret_cast<void*>(b.uc));
+    b = NvlsBuf{};
+    return;
+  }
+  DrvApi* d = drv();
+  if (d) {
+    if (b.mcva) {
+      d->memUnmap(b.mcva, b.size);
+      d->addrFree(b.mcva, b.size);
+    }
+    if (b.uc) {
+      d->memUnmap(b.uc, b.size);
+      d->addrFree(b.uc, b.size);
+    }
+    if (b.mc && b.phys) {
+      CUdevice cud;
+      if (d->devGet(&cud, b.dev) == CUDA_SUCCESS) d->mcUnbind(b.mc, cud, 0, b.size);
+    }
+    if (b.phys) d->memRelease(b.phys);
+    if (b.mc) d->memRelease(b.mc);
+  }
+  b = NvlsBuf{};
+}
+
+// Host-synchronous collective setup (first use, or a larger problem): every
+// rank of the communicator must call it with the same `bytes`.
+lce_status_t nvls_ensure(lce_comm_t c, size_t bytes, cudaStream_t s) {
+  NvlsBuf& b = c->nvls;
+  const bool emulate = nvls_requested() == 2;
+  if (b.ready && b.bytes >= bytes && b.unicast == emulate) return LCE_OK;
+  if (emulate) {  // one rank only: a unicast stand-in for the multicast buffer
+    if (c->nranks != 1) return LCE_ERR_COMM;
+    nvls_release(c);
+    b.size = (bytes + 4096 + 4095) / 4096 * 4096;
+    void* p = nullptr;
+    LCE_CUDA(cudaMalloc(&p, b.size));
+    LCE_CUDA(cudaMemsetAsync(p, 0, b.size, s));
+    b.uc = b.mcva = reinterpret_cast<CUdeviceptr>(p);
+    b.unicast = true;
+    b.bytes = bytes;
+    b.ready = true;
+    return LCE_OK;
+  }
+  DrvApi* d = drv();
+  NcclApi* nc = nccl();
+  if (!d || !nc || !nc->broadcast) return LCE_ERR_CUDA;
+  nvls_release(c);
+  int dev = 0;
+  LCE_CUDA(cudaGetDevice(&dev));
+  CUdevice cud;
+  LCE_CU(d->devGet(&cud, dev));
+  int mc_ok = 0;
+  LCE_CU(d->devAttr(&mc_ok, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cud));
+  if (!c->scratch) LCE_CUDA(cudaMalloc(&c->scratch, 256));
+  // every rank must support multicast (MIN over ranks)
+  int32_t* sc = static_cast<int32_t*>(c->scratch);
+  LCE_CUDA(cudaMemcpyAsync(sc, &mc_ok, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  if (nc->allReduce(sc, sc, 1, ncclInt32, ncclMin, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+  LCE_CUDA(cudaMemcpyAsync(&mc_ok, sc, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  LCE_CUDA(cudaStreamSynchronize(s));
+  if (!mc_ok) return LCE_ERR_DEVICE;
+  CUmulticastObjectProp prop{};
+  prop.numDevices = static_cast<unsigned>(c->nranks);
+  prop.handleTypes = c->nranks > 1 ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
+  size_t gran = 0;
+  prop.size = bytes + 4096;
+  LCE_CU(d->mcGran(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  const size_t size = (bytes + 4096 + gran - 1) / gran * gran;
+  prop.size = size;
+  // rank 0 creates the multicast object; the others import it by duplicating
+  // rank 0's file descriptor (pidfd_getfd); {pid, fd} travel by ncclBroadcast
+  struct {
+    int32_t pid, fd;
+  } ex{static_cast<int32_t>(getpid()), -1};
+  if (c->rank == 0) {
+    // a driver / partition without multicast objects (e.g. a container that
+    // sees one GPU of the NVSwitch fabric) refuses here: LCE_ERR_DEVICE
+    // (a one-rank communicator has no peer to wait for it; with more ranks
+    // the others then fail in the broadcast below -- NCCL path recommended)
+    const CUresult r = d->mcCreate(&b.mc, &prop);
+    if (r != CUDA_SUCCESS) {
+      if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: cuMulticastCreate -> CUresult %d\n", (int)r);
+      b.mc = 0;
+      if (c->nranks == 1) return LCE_ERR_DEVICE;
+      ex.fd = -2;  // tell the other ranks
+    }
+    if (c->nranks > 1 && b.mc) {
+      int fd = -1;
+      LCE_CU(d->exportH(&fd, b.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+      ex.fd = fd;
+    }
+  }
+  if (c->nranks > 1) {
+    LCE_CUDA(cudaMemcpyAsync(sc, &ex, sizeof(ex), cudaMemcpyHostToDevice, s));
+    if (nc->broadcast(sc, sc, sizeof(ex), ncclUint8, 0, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+    LCE_CUDA(cudaMemcpyAsync(&ex, sc, sizeof(ex), cudaMemcpyDeviceToHost, s));
+    LCE_CUDA(cudaStreamSynchronize(s));
+    if (ex.fd == -2) return LCE_ERR_DEVICE;  // rank 0 could not create the multicast object
+    if (c->rank != 0) {
+      const int pidfd = static_cast<int>(syscall(SYS_pidfd_open, ex.pid, 0));
+      if (pidfd < 0) return LCE_ERR_CUDA;
+      const int fd = static_cast<int>(syscall(SYS_pidfd_getfd, pidfd, ex.fd, 0));
+      close(pidfd);
+      if (fd < 0) return LCE_ERR_CUDA;
+      const CUresult r = d->importH(&b.mc, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)),
+                                    CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+      close(fd);
+      LCE_CU(r);
+    }
+  }
+  LCE_CU(d->mcAdd(b.mc, cud));
+  // every device is added before anyone binds memory: a barrier over NCCL
+  if (c->nranks > 1) {
+    if (nc->allReduce(sc, sc, 1, ncclInt32, ncclSum, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+    LCE_CUDA(cudaStreamSynchronize(s));
+  }
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = dev;
+  LCE_CU(d->memCreate(&b.phys, size, &ap, 0));
+  b.size = size;
+  b.dev = dev;
+  LCE_CU(d->mcBind(b.mc, 0, b.phys, 0, size, 0));
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  LCE_CU(d->addrReserve(&b.uc, size, gran, 0, 0));
+  LCE_CU(d->memMap(b.uc, size, 0, b.phys, 0));
+  LCE_CU(d->setAccess(b.uc, size, &acc, 1));
+  LCE_CU(d->addrReserve(&b.mcva, size, gran, 0, 0));
+  LCE_CU(d->memMap(b.mcva, size, 0, b.mc, 0));
+  LCE_CU(d->setAccess(b.mcva, size, &acc, 1));
+  LCE_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(b.uc), 0, size, s));
+  LCE_CUDA(cudaStreamSynchronize(s));
+  if (c->nranks > 1) {  // every copy (and its barrier counter) is zero before first use
+    if (nc->allReduce(sc, sc, 1, ncclInt32, ncclSum, c->comm, s) != ncclSuccess) return LCE_ERR_NCCL;
+    LCE_CUDA(cudaStreamSynchronize(s));
+  }
+  b.bytes = bytes;
+  b.barriers = 0;
+  b.ready = true;
+  return LCE_OK;
+}
+
+// The NVLS fp32 dH buffer of `comm` for this call, or null (NCCL path).
+float* nvls_buffer(lce_comm_t comm, size_t bytes, cudaStream_t s, lce_status_t* st) {
+  *st = LCE_OK;
+  if (!comm || comm->mode != LCE_PAR_VOCAB || !nvls_requested()) return nullptr;
+  *st = nvls_ensure(comm, bytes, s);
+  return *st == LCE_OK ? reinterpret_cast<float*>(comm->nvls.mcva) : nullptr;
+}
+
+// Zero this rank's copy of the first `bytes`, then a barrier so that no rank
+// adds into a copy another rank has not cleared yet.
+lce_status_t nvls_begin(lce_comm_t c, size_t bytes, cudaStream_t s);
+// Barrier over every rank's GPU through the multicast counter (stream-ordered).
+lce_status_t nvls_barrier(lce_comm_t c, cudaStream_t s) {
+  NvlsBuf& b = c->nvls;
+  const uint32_t target = ++b.barriers * static_cast<uint32_t>(c->nranks);
+  uint32_t* mcf = reinterpret_cast<uint32_t*>(b.mcva + b.size - 4096);
+  const uint32_t* ucf = reinterpret_cast<const uint32_t*>(b.uc + b.size - 4096);
+  LaunchScope sc(LCE_K_COMM, s);
+  nvls_barrier_kernel<<<1, 32, 0, s>>>(mcf, ucf, target, b.unicast ? 1 : 0);
+  return last_error();
+}
+lce_status_t nvls_begin(lce_comm_t c, size_t bytes, cudaStream_t s) {
+  LCE_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(c->nvls.uc), 0, bytes, s));
+  return nvls_barrier(c, s);
+}
+// This rank's copy of the reduced buffer (read after the closing barrier).
+float* nvls_local(lce_comm_t c) { return reinterpret_cast<float*>(c->nvls.uc); }
 
 lce_status_t allreduce(lce_comm_t c, void* buf, size_t count, ncclRedOp_t op, cudaStream_t s) {
   NcclApi* api = nccl();
@@ -918,6 +1196,12 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
                                                                gsc, labels, p->ignore_index, p->vocab_total, dhidden);
     LCE_TRY(last_error());
   }
+  // NVLS (LCE_NVLS=1): every vocab chunk's dH epilogue adds into the multicast
+  // buffer, which the switch sums over ranks; one barrier after the last dW
+  lce_status_t nst;
+  float* nvls_mc = multi ? nvls_buffer(comm, static_cast<size_t>(pl.cap * pl.D * 4), s, &nst) : nullptr;
+  if (multi) LCE_TRY(nst);
+  if (nvls_mc) LCE_TRY(nvls_begin(comm, static_cast<size_t>(pl.cap * pl.D * 4), s));
   CUtensorMap t_hc_k, t_hc_mn, t_g_k, t_g_mn;
   LCE_TRY(map_kmajor(&t_hc_k, hc, pl.cap, pl.D, pl.D, BM));
   LCE_TRY(map_mnmajor(&t_hc_mn, hc, pl.cap, pl.D, pl.D));
@@ -945,8 +1229,10 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
       GemmDims d{&hdr->n_valid, 0, nullptr, static_cast<int32_t>(vc), static_cast<int32_t>(pl.D)};
       EpiDH::Params ep{dh, pl.D, k == 0, (!multi && !dh_tma && k == pl.n_chunks - 1) ? 1 : 0, hdr, dhidden, idx,
                        0, 1};
-      ep.use_map = dh_tma ? 1 : 0;
-      if (dh_tma) LCE_TRY(map_f32_store(&ep.map, dh, pl.D, pl.cap, pl.D));
+      ep.use_map = (dh_tma && !nvls_mc) ? 1 : 0;
+      if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dh, pl.D, pl.cap, pl.D));
+      ep.mc_out = nvls_mc;  // unscaled chunk sums into the switch-reduced buffer
+      ep.mc_unicast = (nvls_mc && comm->nvls.unicast) ? 1 : 0;
       // the TMA epilogue is short enough for wide tiles; the read-modify-write
       // one (LCE_DH_TMA=0) is not
       LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, dev.sms, s,
@@ -955,7 +1241,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
     // S7 (vocab-parallel): once the last chunk's dH partial is complete, its
     // all-reduce runs on the communicator's side stream while the last dW GEMM
     // (which does not read dH) runs here.
-    if (multi && k == pl.n_chunks - 1) {
+    if (multi && !nvls_mc && k == pl.n_chunks - 1) {
       LCE_CUDA(cudaEventRecord(comm->dh_ready, s));
       LCE_CUDA(cudaStreamWaitEvent(comm->side, comm->dh_ready, 0));
       LCE_TRY(allreduce(comm, dh, static_cast<size_t>(pl.N * pl.D), ncclSum, comm->side));
@@ -973,7 +1259,7 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
         if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight + v0 * pl.D, pl.D, vc, pl.D));
         ep.prefetch = 0;  // each dW row block is written once here (K = all tokens)
         // the last chunk's dW runs beside the dH all-reduce (vocab-parallel)
-        const int g_sms = (multi && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
+        const int g_sms = (multi && !nvls_mc && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
         LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, g_sms, s,
                                                  pl.cap >= kWideMinRows ? 1 : 0)));
       } else {  // NEXT-2: the AdamW step of these W rows happens in the dW epilogue
@@ -986,12 +1272,17 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
                             static_cast<float>(h.lr / bc1), static_cast<float>(sqrt(bc2))};
         // pair tiles: the optimizer epilogue (26 bytes of state traffic per
         // element) is too long to hide behind the wide kernel's other half
-        const int g_sms = (multi && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
+        const int g_sms = (multi && !nvls_mc && k == pl.n_chunks - 1) ? overlap_sms(comm, dev.sms) : dev.sms;
         LCE_TRY((launch_gemm<true, true, EpiAdamW>(LCE_K_BWD_DW, t_g_mn, t_hc_mn, d, ep, g_sms, s, 0)));
       }
     }
   }
-  if (multi || dh_tma) {
+  if (nvls_mc) {  // every rank's adds have landed in every copy: scale, cast, scatter this rank's copy
+    LCE_TRY(nvls_barrier(comm, s));
+    LaunchScope sc(LCE_K_FINAL, s);
+    finalize_dh_kernel<<<static_cast<unsigned>(pl.N), 256, 0, s>>>(nvls_local(comm), pl.D, idx, hdr, dhidden);
+    LCE_TRY(last_error());
+  } else if (multi || dh_tma) {
     // S7: dH summed over the vocab shards, then scaled, cast, scattered
     if (multi) LCE_CUDA(cudaStreamWaitEvent(s, comm->dh_reduced, 0));
     LaunchScope sc(LCE_K_FINAL, s);
@@ -1010,9 +1301,37 @@ lce_status_t backward_impl(const lce_problem_t* p, lce_comm_t comm_in, const uin
 lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStream_t s, Header* hdr,
                          const CUtensorMap& t_g_k, const CUtensorMap& t_w_mn, const CUtensorMap& t_g_mn,
                          const CUtensorMap& t_h_mn, int32_t r0, float* slab, float* vdh, const int32_t* idx,
-                         uint16_t* dhidden, float* dweight, bool accumulate, const float* row_coef = nullptr) {
+                         uint16_t* dhidden, float* dweight, bool accumulate, const float* row_coef = nullptr,
+                         float* nvls_mc = nullptr) {
   const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
   const int split = fp.split;
+  if (nvls_mc) {
+    // NVLS: the dH GEMM's epilogue adds its (split-K) partials of the chunk rows
+    // into the multicast buffer -- summed over ranks in the switch -- while the
+    // GEMM runs; no slabs, no NCCL kernel, no SMs held back for one
+    const size_t bytes = static_cast<size_t>(fp.Nc * fp.D * 4);
+    LCE_TRY(nvls_begin(comm, bytes, s));
+    {
+      GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
+      EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, nullptr, 0};
+      ep.row_coef = row_coef;
+      ep.mc_out = nvls_mc;
+      ep.mc_unicast = comm->nvls.unicast ? 1 : 0;
+      LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s, fp.wide_dh)));
+    }
+    {
+      GemmDims d{nullptr, Vl, &hdr->n_valid, 0, D, 0, 0, r0, Nc};
+      EpiDW::Params ep{dweight, fp.D, accumulate ? 1 : 0, hdr, 0};
+      ep.use_map = dw_tma();
+      if (ep.use_map) LCE_TRY(map_f32_store(&ep.map, dweight, fp.D, fp.Vl, fp.D));
+      LCE_TRY((launch_gemm<true, true, EpiDW>(LCE_K_BWD_DW, t_g_mn, t_h_mn, d, ep, sms, s, fp.wide_dw)));
+    }
+    LCE_TRY(nvls_barrier(comm, s));  // every rank's partials have landed in every copy
+    LaunchScope sc(LCE_K_FINAL, s);
+    reduce_dh_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(nvls_local(comm), 1, fp.Nc * fp.D, fp.D, r0, Nc, idx,
+                                                                 hdr, dhidden);
+    return last_error();
+  }
   {
     GemmDims d{&hdr->n_valid, 0, nullptr, Vl, D, r0, Nc, 0, 0, split};
     float* part = split > 1 ? slab : (comm ? vdh : nullptr);
@@ -1164,10 +1483,6 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   // (no host sync; under vocab parallelism each rank decides for its own
   // partials).  LCE_FUSED_SCALED=0 selects the fix-up form.
   const bool scaled = !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
-  // one TMEM pass in the forward epilogue (partials relative to the reference;
-  // one GPU or token parallel: under vocab parallelism a rank's fallback could
-  // not redo the cross-rank combine alone).  LCE_FWD_ONEPASS=0: two passes.
-  const bool one_pass = scaled && !comm && !(getenv("LCE_FWD_ONEPASS") && atoi(getenv("LCE_FWD_ONEPASS")) == 0);
   float* qref = reinterpret_cast<float*>(ws + fp.qref);
   float* coef = reinterpret_cast<float*>(ws + fp.coef);
   uint16_t* hs = reinterpret_cast<uint16_t*>(ws + fp.hs);
@@ -1184,6 +1499,9 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   }
   // vocab-parallel: the target row of W lives on one rank (the others add 0)
   if (scaled && comm) LCE_TRY(allreduce(comm, qref, static_cast<size_t>(fp.n_chunks * fp.Nc), ncclSum, s));
+  lce_status_t nst;
+  float* nvls_mc = nvls_buffer(comm, static_cast<size_t>(fp.Nc * fp.D * 4), s, &nst);  // LCE_NVLS=1
+  LCE_TRY(nst);
   for (int64_t q = 0; q < fp.n_chunks; ++q) {
     const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
     const uint16_t* hq = hc + static_cast<int64_t>(r0) * fp.D;
@@ -1198,7 +1516,6 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       ep.store_q = 1;
       ep.q_ref = scaled ? qref : nullptr;
       ep.q_flag = scaled ? qflag : nullptr;
-      ep.one_pass = one_pass ? 1 : 0;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
@@ -1248,12 +1565,6 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       ep.store_q = 1;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_BWD_G, t_h_k, t_w_k, d, ep, dev.sms, s)));
-      if (one_pass) {  // the one-pass partials of a flagged chunk may have overflowed: combine again
-        LaunchScope sc(LCE_K_COMBINE, s);
-        combine_rows_kernel<<<cb, 256, 0, s>>>(pm, ps, static_cast<int>(fp.n_tiles), fp.Nc, r0, Nc, zt, idx, hdr, lse,
-                                              token_loss, lsec, ltok, nullptr, nullptr, redo_rows);
-        LCE_TRY(last_error());
-      }
     }
     {  // S4 without recompute: G = s_i (softmax - onehot) from the kept q, in place
       // (scaled form: only on the fallback)
@@ -1265,7 +1576,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       LCE_TRY(last_error());
     }
     LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_w_mn, t_g_mn, scaled ? t_hs_mn : t_h_mn, r0, slab, vdh,
-                        idx, dhidden, dweight, q > 0 || accumulate_dweight, scaled ? coef : nullptr));
+                        idx, dhidden, dweight, q > 0 || accumulate_dweight, scaled ? coef : nullptr, nvls_mc));
   }
   {
     LaunchScope sc(LCE_K_COMBINE, s);
@@ -1359,6 +1670,9 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in,
   }
   const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
   const int32_t Dt = static_cast<int32_t>(kp.Dt);
+  lce_status_t nst;
+  float* kd_mc = nvls_buffer(comm, static_cast<size_t>(fp.Nc * fp.D * 4), s, &nst);  // LCE_NVLS=1
+  LCE_TRY(nst);
   CUtensorMap t_ws_k, t_wt_k, t_ws_mn, t_g_k, t_g_mn;
   LCE_TRY(map_kmajor(&t_ws_k, weight_s, fp.Vl, fp.D, fp.D, b_box_rows()));
   LCE_TRY(map_kmajor(&t_wt_k, weight_t, fp.Vl, kp.Dt, kp.Dt, b_box_rows()));
@@ -1428,7 +1742,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in,
     }
     // dH_S rows of the chunk and dW_S (student head only; the teacher gets no gradient)
     LCE_TRY(chunk_grads(fp, comm, dev.sms, s, hdr, t_g_k, t_ws_mn, t_g_mn, t_hs_mn, r0, Zs, vdh, idx, dhidden_s,
-                        dweight_s, q > 0 || accumulate_dweight));
+                        dweight_s, q > 0 || accumulate_dweight, nullptr, kd_mc));
   }
   {
     LaunchScope sc(LCE_K_COMBINE, s);
@@ -1481,7 +1795,7 @@ lce_status_t lce_comm_init_mode(lce_comm_t* comm, const uint8_t id[128], int nra
   memcpy(&u, id, 128);
   ncclComm_t c;
   if (api->commInitRank(&c, nranks, u, rank) != ncclSuccess) return LCE_ERR_NCCL;
-  lce_comm_s* cs = new lce_comm_s{c, nranks, rank, mode, nullptr, nullptr, nullptr};
+  lce_comm_s* cs = new lce_comm_s{c, nranks, rank, mode, nullptr, nullptr, nullptr, NvlsBuf{}, nullptr};
   if (cudaStreamCreateWithFlags(&cs->side, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&cs->dh_ready, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&cs->dh_reduced, cudaEventDisableTiming) != cudaSuccess) {
@@ -1502,6 +1816,8 @@ lce_status_t lce_comm_destroy(lce_comm_t comm) {
   NcclApi* api = nccl();
   lce_status_t st = LCE_OK;
   if (api && api->commDestroy(comm->comm) != ncclSuccess) st = LCE_ERR_NCCL;
+  nvls_release(comm);
+  if (comm->scratch) cudaFree(comm->scratch);
   if (comm->side) cudaStreamDestroy(comm->side);
   if (comm->dh_ready) cudaEventDestroy(comm->dh_ready);
   if (comm->dh_reduced) cudaEventDestroy(comm->dh_reduced);

@@ -33,6 +33,12 @@ def main():
             F.backward(h, w, y, o2["lse"], grad_loss=g, reduction="none")
             F.forward_backward(h, w, y, chunk_budget_bytes=256 * 6 * 1024)
             F.forward_backward(h, w, y, comm=comm, chunk_budget_bytes=256 * 6 * 1024)
+            os.environ["LCE_NVLS"] = "2"  # the NVLS dH sequence (one-rank unicast emulation)
+            F.forward_backward(h, w, y, comm=comm, chunk_budget_bytes=256 * 2 * 1024)
+            o3 = F.forward(h, w, y, comm=comm)
+            F.backward(h, w, y, o3["lse"], comm=comm, chunk_budget_bytes=budget)
+            del os.environ["LCE_NVLS"]
+            F.backward(h, w, y, out["lse"], chunk_budget_bytes=budget, dweight_dtype=torch.bfloat16)
             theta = w.float().clone()
             m = torch.zeros_like(theta)
             v = torch.zeros_like(theta)

@@ -77,15 +77,25 @@ def main():
             Hn, Wn, yn = H.float().cpu().numpy(), W.float().cpu().numpy(), y.cpu().numpy()
             o_f = lce_forward(Hn, Wn, yn)
             o_b = lce_backward(Hn, Wn, yn)
-            for path in ("split", "fused"):
-                tag = f"vocab_{path}_N{N}_V{V}"
-                if path == "split":
-                    out = F.forward(H, Wsh, y, comm=cv, vocab_start=v0, vocab_total=V, with_token_loss=True)
-                    dh, dw = F.backward(H, Wsh, y, out["lse"], comm=cv, vocab_start=v0, vocab_total=V)
-                else:
-                    out = F.forward_backward(H, Wsh, y, comm=cv, vocab_start=v0, vocab_total=V, with_token_loss=True,
-                                             chunk_budget_bytes=256 * 2 * 512)
-                    dh, dw = out["dhidden"], out["dweight"]
+            for path, nvls in (("split", 0), ("fused", 0), ("split", 1), ("fused", 1)):
+                tag = f"vocab_{path}{'_nvls' if nvls else ''}_N{N}_V{V}"
+                os.environ["LCE_NVLS"] = str(nvls)  # 1: dH summed in the switch by the GEMM epilogue
+                try:
+                    if path == "split":
+                        out = F.forward(H, Wsh, y, comm=cv, vocab_start=v0, vocab_total=V, with_token_loss=True)
+                        dh, dw = F.backward(H, Wsh, y, out["lse"], comm=cv, vocab_start=v0, vocab_total=V)
+                    else:
+                        out = F.forward_backward(H, Wsh, y, comm=cv, vocab_start=v0, vocab_total=V,
+                                                 with_token_loss=True, chunk_budget_bytes=256 * 2 * 512)
+                        dh, dw = out["dhidden"], out["dweight"]
+                except F.LceError as e:
+                    if nvls and e.code == 7:  # no multicast support on this box: recorded, not failed
+                        if rank == 0:
+                            checks[tag + "_skipped"] = {"ok": True, "info": "multicast unsupported"}
+                        continue
+                    raise
+                finally:
+                    os.environ["LCE_NVLS"] = "0"
                 torch.cuda.synchronize()
                 losses = gather(out["loss"])
                 lses = gather(out["lse"])
@@ -94,7 +104,8 @@ def main():
                 if rank == 0:
                     ok(tag + "_loss_bitwise_across_ranks", all(torch.equal(losses[0], x) for x in losses))
                     ok(tag + "_lse_bitwise_across_ranks", all(torch.equal(lses[0], x) for x in lses))
-                    ok(tag + "_dH_identical_across_ranks", all(torch.equal(dhs[0], x) for x in dhs))
+                    if not nvls:  # NVLS: in-switch order may differ per copy; checked against the oracle
+                        ok(tag + "_dH_identical_across_ranks", all(torch.equal(dhs[0], x) for x in dhs))
                     L = losses[0].item()
                     ok(tag + "_loss", abs(L - o_f["loss"]) <= LOSS_TOL * abs(o_f["loss"]), (L, o_f["loss"]))
                     lerr = float(np.max(np.abs(lses[0].cpu().double().numpy() - o_f["lse"])

@@ -316,6 +316,41 @@ def test_single_rank_communicator_path(cuda_lib):
         comm.close()
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("path", ["split", "fused"])
+def test_nvls_in_switch_dh_reduction_single_rank(cuda_lib, monkeypatch, path, mode):
+    """LCE_NVLS (SURVEY 8e upgrade): the dH GEMM's epilogue adds its
+    partials (split-K items included) into a shared fp32 buffer, an NVLS
+    barrier kernel closes the chunk, the cast / scatter reads the local copy --
+    against the oracle over several row / vocab chunks, twice (the buffer
+    persists on the communicator).
+    mode 1: a real multicast object (cuMulticastCreate / AddDevice / BindMem,
+    multimem.red.add.v4.f32); skips where the driver refuses multicast objects
+    (LCE_ERR_DEVICE -- the one-GPU gpurun containers do, profiles/
+    round2_multicast_probe.log).  mode 2: the same sequence on a unicast
+    buffer with plain red.global.add (one rank), which runs everywhere."""
+    import paper_2605_21442_b200 as F
+
+    monkeypatch.setenv("LCE_NVLS", mode)
+    inp = small(900, 256, 5000, seed=26)
+    lab = inp.labels.cpu().numpy()
+    comm = F.Comm.single()
+    try:
+        for _ in range(2):
+            try:
+                if path == "split":
+                    g = gpu_run(inp, comm=comm, budget=900 * 2 * 1024)
+                else:
+                    g = fused_run(inp, comm=comm, budget=256 * 2 * 5120)
+            except F.LceError as e:
+                if mode == "1" and e.code == 7:
+                    pytest.skip("the driver refuses multicast objects on this box (LCE_ERR_DEVICE)")
+                raise
+            assert_parity(g, oracle_run(inp), lab)
+    finally:
+        comm.close()
+
+
 @pytest.mark.parametrize("reserve", [16, 38])
 def test_communicator_with_reserved_sms(cuda_lib, monkeypatch, reserve):
     """Under vocab parallelism the dW GEMM that overlaps the dH all-reduce runs
