@@ -407,7 +407,8 @@ struct EpiDW : EpiBase {
     int32_t use_map;      // 1: write through `map` (fp32 32x32 boxes, 128B swizzle): TMA store,
                           //    or TMA reduce-add when accumulating (the L2 adds; no read by the SM)
     alignas(64) CUtensorMap map;  // [M rows of this GEMM, D] (rows / cols past it are clipped)
-    int32_t dbg;                  // A/B diagnostics: 1 skip the writes, 2 also the TMEM reads
+    int32_t dbg;                  // A/B diagnostics: 1 skip the writes, 2 also the TMEM reads,
+                                  // 3 / 4 skip the writes of accumulating / overwriting launches only
     uint16_t* dw_bf16;            // non-null: write bf16(c * acc) rows here instead (LCE_DW_BF16,
                                   // overwrite only; the direct path)
     int32_t prefetch;             // accumulate + TMA: L2 prefetch of the old dW rows
@@ -426,8 +427,8 @@ struct EpiDW : EpiBase {
   }
   static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
     if (t.zero_acc && p.accumulate) return;  // K == 0 adds nothing (uniform across the CTA)
-    if (p.dbg) {
-      if (p.dbg == 1) {
+    if (p.dbg == 1 || p.dbg == 2 || (p.dbg == 3 && p.accumulate) || (p.dbg == 4 && !p.accumulate)) {
+      if (p.dbg != 2) {
         float x[32];
         for (int c = 0; c < BN / 32; ++c) load_chunk(taddr, c, false, x);
         if (x[0] == 12345.f) *p.dW = x[1];  // keep the loads
@@ -698,6 +699,10 @@ __global__ void __launch_bounds__(1024) prep_kernel(const int32_t* __restrict__ 
     __syncthreads();
   }
   const int any_bad = __syncthreads_or(bad_any ? 1 : 0);
+  // target logits of the padding rows [N_v, ceil256(N)) are defined too (0):
+  // the vocab-parallel exchange copies all of them
+  if (zt)
+    for (int i = base_s + tid; i < ((N + 255) & ~255); i += 1024) zt[i] = 0.f;
   if (tid == 0) {
     hdr->status = any_bad ? kStatusBadLabel : 0u;
     const int nv = base_s;
