@@ -94,7 +94,6 @@ struct TileInfo {
   uint8_t* smem;  // this warp's kEpiBufs x 4 KB epilogue staging tiles (1 KB aligned)
   uint32_t nst;   // TMA stores this warp has issued so far (selects the next staging tile)
   uint64_t st_policy;  // L2 cache policy for the epilogue's TMA stores
-  uint32_t nbuf;       // staging tiles of this warp: 1, or 2 (0 means 2)
 };
 
 // This warp's next staging tile: waits (lane 0) until the store that last read
@@ -102,12 +101,6 @@ struct TileInfo {
 // reading.  Every call must be followed by exactly one committed store group.
 __device__ __forceinline__ uint8_t* stage_next(TileInfo& t) {
   static_assert(kEpiBufs == 2, "wait depth below assumes two staging tiles");
-  if (t.nbuf == 1) {  // one staging tile: the previous store must be done reading it
-    if ((t.row & 31) == 0) tma_store_wait_read();
-    __syncwarp();
-    ++t.nst;
-    return t.smem;
-  }
   if ((t.row & 31) == 0) tma_store_wait_read_1();
   __syncwarp();
   uint8_t* st = t.smem + (t.nst & (kEpiBufs - 1)) * kEpiWarpSmem;
@@ -532,14 +525,9 @@ constexpr int kWideStages = 4;
 constexpr int kWideAStage = 256 * BK * 2;  // 32 KB
 constexpr int kWideBStage = 128 * BK * 2;  // 16 KB
 constexpr int kWideSmemBytes = kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + kEpiSmemBytes;
-// Split epilogue (launched with kWideSplitThreads): warps 4-7 drain accumulator
-// half 0 and warps 8-11 half 1, each with one 4 KB staging tile (the same
-// shared memory as 4 warps x 2 tiles), so half 1's drain starts as soon as
-// its last MMA retires instead of after half 0's drain.
-constexpr int kWideSplitThreads = 384;
 
 template <bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(kWideSplitThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_wide_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const GemmDims dims, const __grid_constant__ typename Epi::Params ep) {
   extern __shared__ uint8_t smem_raw[];
@@ -699,31 +687,7 @@ __global__ void __launch_bounds__(kWideSplitThreads, 1)
         acc_phase ^= 1;
       }
     }
-  } else if (warp >= 4 && blockDim.x == kWideSplitThreads) {
-    // ------------------------------------------------------------ split epilogue (both CTAs)
-    const int q = warp & 3;
-    const int h = (warp - 4) >> 2;  // the accumulator half this warp drains
-    uint32_t acc_phase = 0;
-    uint32_t nst = 0;
-    const uint64_t stp = l2_policy(dims.st_hint);
-    for (int t = cluster; t < num_tiles; t += nclusters) {
-      const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-      const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank) + 128 * h;
-      TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + (warp - 4) * kEpiWarpSmem, nst, stp, 1};
-      Epi::prefetch(ep, ti);
-      mbar_wait_cluster(&tfull[h], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + h * BN + (static_cast<uint32_t>(q * 32) << 16);
-      Epi::apply(ep, taddr, ti);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tempty[h], 0);
-      nst = ti.nst;
-      acc_phase ^= 1;
-    }
-    Epi::finish(ep);
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;
     uint32_t acc_phase = 0;

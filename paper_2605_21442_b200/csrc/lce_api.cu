@@ -571,12 +571,7 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool wide = use_wide(cls, wide_pref) != 0;
-  if (wide) {
-    cfg.dynamicSmemBytes = kWideSmemBytes;
-    // LCE_WIDE_SPLIT=1: one warp group per accumulator half (gemm.cuh)
-    const char* e = getenv("LCE_WIDE_SPLIT");
-    if (e && atoi(e) == 1) cfg.blockDim = dim3(kWideSplitThreads);
-  }
+  if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
   cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
                        : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
   if (e != cudaSuccess) {

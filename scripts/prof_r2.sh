@@ -1,11 +1,13 @@
-# r2 profile: fused path (default) + split path, launch lists and one full capture per GEMM class
-set -x
+# round-2 ncu evidence (run under gpurun):  bash scripts/prof_r2.sh
+#   launch lists (gpu__time_duration, serialised) of the 8B fused and split steps (2 steps each),
+#   --set full of every kernel class of one fused 8B row chunk and of the split path's GEMMs
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity.py -q -m gpu 2>&1 | tail -4
-python bench.py --steps 10 --warmup 3 --chunk-budget 8589934592 --no-cpu-baseline --no-e2e 2>&1 | tail -1
-python bench.py --steps 10 --warmup 3 --path split --no-cpu-baseline --no-e2e 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_r2_fused.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gemm_pair_kernel -c 4 -o gpurun_out/prof_r2_fused python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_r2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:gemm_pair_kernel -c 4 -o gpurun_out/prof_r2_split python bench.py --steps 1 --warmup 0 --path split --no-cpu-baseline --no-e2e > gpurun_out/ncu_r2s.log 2>&1
-python bench.py --steps 10 --warmup 3 > gpurun_out/bench_r2.log 2>&1
-tail -1 gpurun_out/bench_r2.log
+python paper_2605_21442_b200/build.py > /dev/null
+S="python scripts/one_step.py --config llama8b --steps 2"
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/round2_fused_launches.csv $S --path fused > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/round2_split_launches.csv $S --path split > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_|combine_rows|scaled_prep|target_dot|reduce_dh" -c 9 \
+    -o gpurun_out/round2_fused python scripts/one_step.py --config llama8b --path fused > gpurun_out/round2_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"gemm_" -c 4 \
+    -o gpurun_out/round2_split python scripts/one_step.py --config llama8b --path split >> gpurun_out/round2_ncu.log 2>&1
+tail -n 3 gpurun_out/round2_ncu.log
