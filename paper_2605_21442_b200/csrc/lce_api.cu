@@ -1516,6 +1516,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       ep.store_q = 1;
       ep.q_ref = scaled ? qref : nullptr;
       ep.q_flag = scaled ? qflag : nullptr;
+      ep.dbg = getenv("LCE_DBG_FWD") ? atoi(getenv("LCE_DBG_FWD")) : 0;
       LCE_TRY(encode_map(&ep.zmap, G, fp.ldv, fp.Nc, fp.ldv, 32));
       LCE_TRY((launch_gemm<false, false, EpiLse>(LCE_K_FWD, t_h_k, t_w_k, d, ep, dev.sms, s)));
     }
