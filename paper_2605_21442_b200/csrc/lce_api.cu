@@ -311,8 +311,16 @@ lce_status_t device_info(DevInfo* out) {
   static bool have[64];
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
+  // LCE_SMS=n (tests, A/B): run every grid on n < #SMs SMs, as on a partial
+  // part (MIG, a reserved slice); the plan's split-K is re-derived for it
+  auto limit = [](DevInfo* d) {
+    const char* e = getenv("LCE_SMS");
+    const int v = e ? atoi(e) : 0;
+    if (v >= 2 && v < d->sms) d->sms = v & ~1;
+  };
   if (dev < 64 && have[dev]) {
     *out = cache[dev];
+    limit(out);
     return out->ok ? LCE_OK : LCE_ERR_DEVICE;
   }
   int major = 0, minor = 0, sms = 0;
@@ -342,6 +350,7 @@ lce_status_t device_info(DevInfo* out) {
     have[dev] = true;
   }
   *out = d;
+  limit(out);
   return d.ok ? LCE_OK : LCE_ERR_DEVICE;
 }
 
