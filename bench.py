@@ -369,7 +369,10 @@ def main():
     dev = torch.device("cuda", local)
     dist = None
     comm = None
-    if world > 1:
+    # LCE_BENCH_FORCE_COMM=1 (tests): the multi-rank plumbing -- process group,
+    # NCCL id broadcast, the library's communicator, max-over-ranks timing --
+    # also at WORLD_SIZE=1, so it is exercised on a one-GPU box
+    if world > 1 or os.environ.get("LCE_BENCH_FORCE_COMM") == "1":
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)

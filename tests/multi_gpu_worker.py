@@ -170,7 +170,7 @@ def main():
         # a bad label on one rank only (one that holds rows): every rank's loss is
         # NaN and every rank reports it, also the rank without rows
         yb = y.clone()
-        if rank == (0 if world == 2 else 1) and yb.numel():
+        if rank == (0 if world <= 2 else 1) and yb.numel():
             yb[0] = V + 5
         ws = F.Workspace()
         out = F.forward(H, inp.weight, yb, comm=ct, workspace=ws)

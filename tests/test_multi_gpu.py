@@ -28,8 +28,11 @@ def _free_port():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
 def test_multi_rank_parity(cuda_lib, P, tmp_path):
+    """P = 1 runs on every box: the same worker under torch.distributed.run with
+    one rank (process-group plumbing, the NCCL id broadcast, the library's
+    communicators and every check's code path); P > 1 needs that many GPUs."""
     import torch
 
     if torch.cuda.device_count() < P:
@@ -44,7 +47,7 @@ def test_multi_rank_parity(cuda_lib, P, tmp_path):
     assert res["world"] == P
     bad = {k: v for k, v in res["checks"].items() if not v["ok"]}
     assert not bad, bad
-    assert len(res["checks"]) >= 30
+    assert len(res["checks"]) >= (20 if P == 1 else 30)
 
 
 def test_bench_multi_gpu_fails_loudly_without_gpus():
@@ -64,3 +67,19 @@ def test_bench_rejects_world_size_mismatch():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
                        capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
     assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
+@pytest.mark.gpu
+def test_bench_multi_rank_plumbing_one_rank(cuda_lib):
+    """bench.py's multi-rank code (process group, communicator, per-step
+    max-over-ranks, the split sub-record and e2e through the communicator)
+    under torch.distributed.run with one rank (LCE_BENCH_FORCE_COMM=1) at a
+    small config: one JSON line with n_gpus 1 and a positive value."""
+    env = dict(os.environ, LCE_BENCH_FORCE_COMM="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "1", "--config", "llama1b", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["split"]["value"] > 0 and line["e2e"]["value"] > 0
