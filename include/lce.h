@@ -285,6 +285,16 @@ lce_status_t lce_comm_destroy(lce_comm_t comm);
 int lce_comm_size(lce_comm_t comm);
 int lce_comm_rank(lce_comm_t comm);
 int lce_comm_mode(lce_comm_t comm); /* lce_parallel_t; LCE_PAR_VOCAB for NULL */
+/* NVLS (environment LCE_NVLS=1, vocab-parallel communicators): the dH
+ * partials are added by the dH GEMM's epilogue into an NVSwitch multicast
+ * buffer owned by the communicator (multimem.red.add; the switch sums the
+ * ranks), replacing the NCCL dH all-reduce, its side stream and the SMs held
+ * back for it.  The first call per problem size sets the buffer up
+ * (cuMulticastCreate / AddDevice / BindMem, host-synchronous, collective over
+ * the communicator); LCE_ERR_DEVICE if any rank's device or driver offers no
+ * multicast objects.  dH is then not bitwise reproducible (in-switch order).
+ * LCE_NVLS=2 runs the same sequence on a unicast buffer (one rank; tests). */
+
 /* Polls ncclCommGetAsyncError: LCE_ERR_NCCL if the communicator hit an
  * asynchronous error (a peer died, a network failure) -- the collectives of
  * the calls above would otherwise block forever -- LCE_OK otherwise (also for
