@@ -56,8 +56,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: tuple = ()) -> str:
+    """`out` / `defines` (-D flags): A/B builds of compile-time variants
+    (scripts/build_variant.py); the package always loads `LIB`."""
+    if out == LIB and not defines and not force and up_to_date():
         return LIB
     cmd = [
         nvcc(),
@@ -67,7 +69,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         "-shared",
         "-I", os.path.join(ROOT, "include"),
         "-I", _nccl_include(),
-        "-o", LIB + ".tmp",
+        *[f"-D{d}" for d in defines],
+        "-o", out + ".tmp",
         *SOURCES,
         "-ldl",
     ]
@@ -75,8 +78,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

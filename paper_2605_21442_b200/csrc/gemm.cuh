@@ -12,6 +12,7 @@
 //   warp 0      TMA producer (one elected lane): A/B k-blocks -> smem ring
 //   warp 1      MMA issuer (one lane): tcgen05.mma 128x256x16, fp32 accum in TMEM
 //   warp 2      TMEM allocator (512 columns = 2 accumulator buffers of 256)
+//   warp 3      (CTA-pair kernels, K-lockstep on) progress monitor, see lockstep_monitor
 //   warps 4..7  epilogue: tcgen05.ld the accumulator (thread = one tile row =
 //               one TMEM lane) while the MMA warp fills the other buffer.
 // Pipelines: smem full/empty mbarriers (TMA <-> MMA, kStages deep) and TMEM
@@ -73,7 +74,75 @@ struct GemmDims {
   // profiler (null = off): CTA 0 records {globaltimer, clock64} at start and
   // end, i.e. the SM clock the kernel actually ran at inside the step
   unsigned long long* probe;
+  // K-lockstep (null = off): the leader CTA of every cluster publishes how
+  // many k-block steps its producer has issued ({lock_gen, steps} in
+  // lock_prog[cluster]) and its producer waits while it is more than lock_d
+  // steps ahead of the slowest cluster, so clusters that share an operand
+  // k-slab read it within a short window, while it is in L2.
+  unsigned long long* lock_prog;
+  uint32_t lock_gen;
+  int32_t lock_d;
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// The K-lockstep is split between two warps of the leader CTA so that no
+// global memory latency sits on the TMA producer's path:
+//   * the producer (lockstep_gate) keeps its issued k-block count in shared
+//     memory and, before each step, waits while it is more than lock_d steps
+//     ahead of the slowest cluster as last seen by the monitor;
+//   * the monitor (warp 3, otherwise idle; lockstep_monitor) publishes this
+//     cluster's count to lock_prog[cluster] and polls every cluster's count
+//     (one load per lane) about once a microsecond until the producer is done.
+// A cluster that is not running makes the gate time out, after which that
+// producer stops waiting for the rest of the launch: the lockstep can delay a
+// producer, never block it.  The peer CTA's producer is paced by the shared
+// stage ring and needs no gate.
+constexpr unsigned long long kLockTimeoutNs = 40000;
+struct LockSmem {
+  uint32_t steps;    // k-block steps the leader's producer has issued
+  uint32_t slowest;  // min over clusters of their published steps (monitor)
+  uint32_t done;     // producer finished
+};
+
+__device__ __forceinline__ void lockstep_gate(const GemmDims& d, volatile LockSmem* ls, uint32_t steps, bool& on) {
+  ls->steps = steps;
+  if (!on || steps <= ls->slowest + static_cast<uint32_t>(d.lock_d)) return;
+  const unsigned long long t0 = globaltimer_ns();
+  while (steps > ls->slowest + static_cast<uint32_t>(d.lock_d)) {
+    if (globaltimer_ns() - t0 > kLockTimeoutNs) {  // a cluster is not running: stop waiting
+      on = false;
+      return;
+    }
+    __nanosleep(64);
+  }
+}
+
+__device__ __forceinline__ void lockstep_monitor(const GemmDims& d, volatile LockSmem* ls, int cluster,
+                                                 int nclusters, int lane) {
+  const unsigned long long tag = static_cast<unsigned long long>(d.lock_gen) << 32;
+  for (;;) {
+    const uint32_t done = __shfl_sync(0xffffffffu, ls->done, 0);
+    const uint32_t mine = done ? 0xffffffffu : ls->steps;
+    if (lane == 0)
+      asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(d.lock_prog + cluster), "l"(tag | mine) : "memory");
+    if (done) return;
+    uint32_t mn = 0xffffffffu;
+    for (int c = lane; c < nclusters; c += 32) {
+      unsigned long long v;
+      asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(d.lock_prog + c));
+      const uint32_t st = (v >> 32) == d.lock_gen ? static_cast<uint32_t>(v) : 0u;
+      mn = st < mn ? st : mn;
+    }
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    if (lane == 0) ls->slowest = mn;
+    __nanosleep(256);
+  }
+}
 
 __device__ __forceinline__ void probe_mark(unsigned long long* probe, int at) {
   if (probe && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -352,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kPairStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile LockSmem* lsm = reinterpret_cast<volatile LockSmem*>(tmem_slot + 4);
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
@@ -370,6 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
   const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
+  // K-lockstep: gate in the leader's producer, monitor in its warp 3
+  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -382,6 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[s], 1);   // multicast commit
       mbar_init(&tempty[s], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
+    lsm->steps = 0;
+    lsm->slowest = 0;
+    lsm->done = 0;
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -400,11 +475,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
+      uint32_t steps = 0;
+      bool lock_on = lock;
       for (int t = cluster; t < num_tiles; t += nclusters) {
         const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         const int ma = w.mb * kPairBM + 128 * rank;  // this CTA's A rows
         const int nbh = w.nb * BN + 128 * rank;      // this CTA's B rows (N half)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          if (lock) lockstep_gate(dims, lsm, steps++, lock_on);
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
           uint8_t* a = sA + stage * kHalf;
@@ -428,7 +506,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (lock) lsm->done = 1;
     }
+  } else if (warp == 3) {
+    if (lock) lockstep_monitor(dims, lsm, cluster, nclusters, lane);
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer (leader only)
@@ -539,6 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kWideStages;  // [2]: accumulator half computed
   uint64_t* tempty = tfull + 2;           // [2]: accumulator half drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  volatile LockSmem* lsm = reinterpret_cast<volatile LockSmem*>(tmem_slot + 4);
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
@@ -557,6 +639,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
   const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
+  // K-lockstep: gate in the leader's producer, monitor in its warp 3
+  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -569,6 +653,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[h], 1);   // multicast commit
       mbar_init(&tempty[h], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
+    lsm->steps = 0;
+    lsm->slowest = 0;
+    lsm->done = 0;
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -587,11 +674,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
+      uint32_t steps = 0;
+      bool lock_on = lock;
       for (int t = cluster; t < num_tiles; t += nclusters) {
         const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
         const int ma = w.mb * kWideBM + 256 * rank;  // this CTA's 256 A rows
         const int nbh = w.nb * BN + 128 * rank;      // this CTA's B rows (N half)
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          if (lock) lockstep_gate(dims, lsm, steps++, lock_on);
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * (kWideAStage + kWideBStage));
           uint8_t* a = sA + stage * kWideAStage;
@@ -616,7 +706,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (lock) lsm->done = 1;
     }
+  } else if (warp == 3) {
+    if (lock) lockstep_monitor(dims, lsm, cluster, nclusters, lane);
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------------------------------------------------- MMA issuer (leader only)

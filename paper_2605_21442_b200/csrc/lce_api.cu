@@ -343,6 +343,9 @@ lce_status_t device_info(DevInfo* out) {
     LCE_SMEM_ATTR(false, true, EpiStore);
     LCE_SMEM_ATTR(true, false, EpiStore);
     LCE_SMEM_ATTR(true, true, EpiStore);
+    LCE_SMEM_ATTR(false, false, EpiDW);  // lce_debug_gemm under LCE_DEBUG_GEMM_TMA
+    LCE_SMEM_ATTR(false, true, EpiDW);
+    LCE_SMEM_ATTR(true, false, EpiDW);
 #undef LCE_SMEM_ATTR
   }
   if (dev < 64) {
@@ -540,6 +543,35 @@ int use_wide(int cls, int dflt) {
   return dflt;
 }
 
+// K-lockstep of the persistent wide-tile grids (gemm.cuh lockstep_gate /
+// lockstep_monitor): one progress word per cluster in a device-global array;
+// every launch gets a new generation tag, so words left by earlier launches
+// read as "not started".  Measured (one B200, in-step, medians of 4-5): the
+// fused step +1.3% at 8B and +4.7% at 70B (the dH / dW GEMMs' DRAM reads
+// drop from 12.6 / 13.9 to 6.2 / 6.7 GB per 8B chunk, cold-cache ncu); on
+// the short-K pair-tile GEMMs (1B dW: -17%) the gate's stalls cost more than
+// the traffic it saves, so it is on for wide tiles only.  LCE_LOCK[_<class>]
+// = 0 / 1 overrides, LCE_LOCK_D sets the allowed drift in k-block steps.
+__device__ unsigned long long g_lock_prog[128];
+constexpr int kLockD = 16;
+void lockstep_config(GemmDims& d, int cls, bool wide) {
+  static std::atomic<uint32_t> gen{0x5a5a0000u};
+  char name[32];
+  snprintf(name, sizeof(name), "LCE_LOCK_%d", cls);
+  const char* env = getenv(name);
+  if (!env) env = getenv("LCE_LOCK");
+  if (!(env ? atoi(env) != 0 : wide)) return;
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_lock_prog) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const int dd = getenv("LCE_LOCK_D") ? atoi(getenv("LCE_LOCK_D")) : kLockD;
+  d.lock_prog = static_cast<unsigned long long*>(p);
+  d.lock_gen = ++gen;
+  d.lock_d = dd < 0 ? 0 : dd;
+}
+
 // wide_pref: this call site's tile shape (0: 256 x 256 pair tiles, 1: 512 x 256
 // wide tiles); environment overrides win.
 template <bool A_MN, bool B_MN, class Epi>
@@ -567,6 +599,8 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
     gemm_kernel<A_MN, B_MN, Epi><<<sms, kThreads, kSmemBytes, s>>>(a, b, d, ep);
     return last_error();
   }
+  const bool wide = use_wide(cls, wide_pref) != 0;
+  if ((sms >> 1) <= 128) lockstep_config(d, cls, wide);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(sms & ~1));
   cfg.blockDim = dim3(kThreads);
@@ -579,7 +613,6 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const bool wide = use_wide(cls, wide_pref) != 0;
   if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
   cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
                        : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
@@ -1910,6 +1943,19 @@ lce_status_t lce_debug_gemm(const uint16_t* A, const uint16_t* B, float* C, int6
   if (b_mn) LCE_TRY(map_mnmajor(&tb, B, K, N, N));
   else LCE_TRY(map_kmajor(&tb, B, N, K, K, b_box_rows()));
   GemmDims d{nullptr, static_cast<int32_t>(M), nullptr, static_cast<int32_t>(K), static_cast<int32_t>(N)};
+  if (getenv("LCE_DEBUG_GEMM_TMA") && N % 4 == 0) {
+    // diagnostics (scripts/gemm_power.py): the dW epilogue's TMA-store drain
+    // instead of EpiStore's scalar stores, so the GEMM runs at mainloop speed
+    // (the raster / hint defaults of kernel class LCE_DEBUG_GEMM_CLS, default the forward's)
+    EpiDW::Params ep{C, N, 0, nullptr, 0};
+    ep.use_map = 1;
+    LCE_TRY(map_f32_store(&ep.map, C, N, M, N));
+    const int cls = getenv("LCE_DEBUG_GEMM_CLS") ? atoi(getenv("LCE_DEBUG_GEMM_CLS")) : LCE_K_FWD;
+    if (!a_mn && !b_mn) return launch_gemm<false, false, EpiDW>(cls, ta, tb, d, ep, dev.sms, s);
+    if (!a_mn && b_mn) return launch_gemm<false, true, EpiDW>(cls, ta, tb, d, ep, dev.sms, s);
+    if (a_mn && !b_mn) return launch_gemm<true, false, EpiDW>(cls, ta, tb, d, ep, dev.sms, s);
+    return launch_gemm<true, true, EpiDW>(cls, ta, tb, d, ep, dev.sms, s);
+  }
   EpiStore::Params ep{C, N};
   if (!a_mn && !b_mn) return launch_gemm<false, false, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);
   if (!a_mn && b_mn) return launch_gemm<false, true, EpiStore>(LCE_K_FWD, ta, tb, d, ep, dev.sms, s);

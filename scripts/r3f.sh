@@ -1,0 +1,7 @@
+# K-lockstep of the persistent GEMM grids: parity, then A/B (LCE_LOCK=0 / E,D)
+python paper_2605_21442_b200/build.py >/dev/null
+timeout 900 python -m pytest tests -m gpu -x -q -k "debug_gemm or fused_many or random_shapes or tiny_config or fused_config_shapes or graph" 2>&1 | tail -2
+timeout 600 python scripts/gemm_power.py --shapes dw,dh --arms wide,pair --seconds 3 | grep -v '^{'
+LCE_LOCK=0 timeout 600 python scripts/gemm_power.py --shapes dw,dh --arms wide,pair --seconds 3 | grep -v '^{'
+timeout 900 python scripts/sweep_env.py --config llama8b --path fused --reps 3 '' 'LCE_LOCK=0' 'LCE_LOCK_E=8 LCE_LOCK_D=32' 'LCE_LOCK_E=32 LCE_LOCK_D=128'
+timeout 900 python scripts/sweep_env.py --config llama8b --path split --reps 3 '' 'LCE_LOCK=0' 'LCE_LOCK_E=8 LCE_LOCK_D=32'

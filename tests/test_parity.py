@@ -277,6 +277,25 @@ def test_deterministic_rerun(cuda_lib):
     assert a["loss"] == b["loss"]
 
 
+@pytest.mark.parametrize("lock", ["0", "1"])
+@pytest.mark.parametrize("path", ["fused", "split"])
+def test_k_lockstep_is_timing_only(cuda_lib, monkeypatch, lock, path):
+    """The K-lockstep of the persistent grids (LCE_LOCK; on by default for wide
+    tiles) only delays TMA producers: forcing it on every GEMM (pair tiles too,
+    a tight drift bound) or off leaves every output bitwise equal to the
+    default schedule (whose parity the other tests check)."""
+    inp = small(16384, 256, 5000, seed=34, ignore_frac=0.1)
+    run = fused_run if path == "fused" else (lambda i: gpu_run(i))
+    monkeypatch.delenv("LCE_LOCK", raising=False)
+    ref = run(inp)
+    monkeypatch.setenv("LCE_LOCK", lock)
+    monkeypatch.setenv("LCE_LOCK_D", "2")
+    got = run(inp)
+    for k in ("lse", "tok", "dH", "dW"):
+        np.testing.assert_array_equal(ref[k], got[k])
+    assert ref["loss"] == got["loss"]
+
+
 @pytest.mark.parametrize("gemm", ["default", "pair"])
 def test_fused_deterministic_and_mask_first(cuda_lib, monkeypatch, gemm):
     """H8 and P3 for the fused path at a shape that takes its wide dH / dW tiles
