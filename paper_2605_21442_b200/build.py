@@ -56,10 +56,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: tuple = ()) -> str:
-    """`out` / `defines` (-D flags): A/B builds of compile-time variants
+def build(force: bool = False, verbose: bool = False, dest: str = LIB, defines: tuple = ()) -> str:
+    """`dest` / `defines` (-D flags): A/B builds of compile-time variants
     (scripts/build_variant.py); the package always loads `LIB`."""
-    if out == LIB and not defines and not force and up_to_date():
+    if dest == LIB and not defines and not force and up_to_date():
         return LIB
     cmd = [
         nvcc(),
@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: t
         "-I", os.path.join(ROOT, "include"),
         "-I", _nccl_include(),
         *[f"-D{d}" for d in defines],
-        "-o", out + ".tmp",
+        "-o", dest + ".tmp",
         *SOURCES,
         "-ldl",
     ]
@@ -78,8 +78,8 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines: t
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(out + ".tmp", out)
-    return out
+    os.replace(dest + ".tmp", dest)
+    return dest
 
 
 if __name__ == "__main__":

@@ -11,4 +11,4 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 spec = importlib.util.spec_from_file_location("lce_build", os.path.join(ROOT, "paper_2605_21442_b200", "build.py"))
 mod = importlib.util.module_from_spec(spec)
 spec.loader.exec_module(mod)
-print(mod.build(force=True, out=os.path.abspath(sys.argv[1]), defines=tuple(sys.argv[2:])))
+print(mod.build(force=True, dest=os.path.abspath(sys.argv[1]), defines=tuple(sys.argv[2:])))
