@@ -546,7 +546,9 @@ int use_wide(int cls, int dflt) {
 // K-lockstep of the persistent wide-tile grids (gemm.cuh lockstep_gate /
 // lockstep_monitor): one progress word per cluster in a device-global array;
 // every launch gets a new generation tag, so words left by earlier launches
-// read as "not started".  Measured (one B200, in-step, medians of 4-5): the
+// read as "not started" (a CUDA-graph replay reuses its captured tag: for the
+// first microsecond, until every monitor has published again, words left by
+// the previous replay read as "done" and gate nothing -- timing only).  Measured (one B200, in-step, medians of 4-5): the
 // fused step +1.3% at 8B and +4.7% at 70B (the dH / dW GEMMs' DRAM reads
 // drop from 12.6 / 13.9 to 6.2 / 6.7 GB per 8B chunk, cold-cache ncu); on
 // the short-K pair-tile GEMMs (1B dW: -17%) the gate's stalls cost more than
