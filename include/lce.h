@@ -30,6 +30,11 @@
  *    outputs untouched.  CUDA launch errors return LCE_ERR_CUDA.
  *  - Results do not depend on the chunk budget beyond fp32 rounding order.
  *  - Calls on different streams with different workspaces are independent.
+ *    (The library image holds one small device-global array, the per-cluster
+ *    k-block progress of its persistent wide-tile GEMMs -- the K-lockstep,
+ *    DESIGN.md section 5.  It only ever delays a TMA producer, tagged per
+ *    launch; GEMMs running concurrently on other streams can make a gate
+ *    time out, which costs time, never results.)
  */
 #ifndef LCE_H_
 #define LCE_H_
