@@ -553,7 +553,7 @@ int use_wide(int cls, int dflt) {
 // drop from 12.6 / 13.9 to 6.2 / 6.7 GB per 8B chunk, cold-cache ncu); on
 // the short-K pair-tile GEMMs (1B dW: -17%) the gate's stalls cost more than
 // the traffic it saves, so it is on for wide tiles only.  LCE_LOCK[_<class>]
-// = 0 / 1 overrides, LCE_LOCK_D sets the allowed drift in k-block steps.
+// = 0 / 1 overrides, LCE_LOCK_D[_<class>] sets the allowed drift in k-block steps.
 __device__ unsigned long long g_lock_prog[128];
 constexpr int kLockD = 16;
 void lockstep_config(GemmDims& d, int cls, bool wide) {
@@ -568,7 +568,10 @@ void lockstep_config(GemmDims& d, int cls, bool wide) {
     cudaGetLastError();
     return;
   }
-  const int dd = getenv("LCE_LOCK_D") ? atoi(getenv("LCE_LOCK_D")) : kLockD;
+  snprintf(name, sizeof(name), "LCE_LOCK_D_%d", cls);
+  const char* de = getenv(name);
+  if (!de) de = getenv("LCE_LOCK_D");
+  const int dd = de ? atoi(de) : kLockD;
   d.lock_prog = static_cast<unsigned long long*>(p);
   d.lock_gen = ++gen;
   d.lock_d = dd < 0 ? 0 : dd;
