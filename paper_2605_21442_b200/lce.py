@@ -59,9 +59,17 @@ class Workspace:
 _default_ws: dict = {}
 
 
-def _ws_for(ws: Optional[Workspace], problem: Problem, device) -> torch.Tensor:
+def _default_workspace(device, tag: str = "", stream=None) -> Workspace:
+    """The default workspace of (device, the call's stream[, entry point]):
+    calls on different streams never share scratch (a shared buffer would race)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = f"{device}{':' + tag if tag else ''}@{s.cuda_stream}"
+    return _default_ws.setdefault(key, Workspace())
+
+
+def _ws_for(ws: Optional[Workspace], problem: Problem, device, stream=None) -> torch.Tensor:
     if ws is None:
-        ws = _default_ws.setdefault(str(device), Workspace())
+        ws = _default_workspace(device, stream=stream)
     need = workspace_bytes(problem)
     if need == 0:
         raise ValueError("invalid LCE problem shape")
@@ -179,7 +187,7 @@ def forward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, *,
     prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
-    ws = _ws_for(workspace, prob, dev)
+    ws = _ws_for(workspace, prob, dev, stream)
     if out is None:
         out = {
             "loss": torch.empty(1, dtype=torch.float32, device=dev),
@@ -213,7 +221,7 @@ def backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Tensor, l
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
     dev = hidden.device
     _check_tensor(lse, "lse", torch.float32, (N,), dev)
-    ws = _ws_for(workspace, prob, dev)
+    ws = _ws_for(workspace, prob, dev, stream)
     if dhidden is None:
         dhidden = torch.empty_like(hidden)
     if dweight is None:
@@ -245,7 +253,7 @@ def backward_adamw(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.Ten
     _check_tensor(lse, "lse", torch.float32, (N,), dev)
     prob = make_problem(N, D, Vl, vocab_start=vocab_start, vocab_total=vocab_total,
                         ignore_index=ignore_index, reduction=reduction, chunk_budget_bytes=chunk_budget_bytes)
-    ws = _ws_for(workspace, prob, dev)
+    ws = _ws_for(workspace, prob, dev, stream)
     if dhidden is None:
         dhidden = torch.empty_like(hidden)
     _check_tensor(dhidden, "dhidden", torch.bfloat16, (N, D), dev)
@@ -282,7 +290,7 @@ def forward_backward(hidden: torch.Tensor, weight: torch.Tensor, labels: torch.T
     if need == 0:
         raise ValueError("invalid LCE problem shape")
     if workspace is None:
-        workspace = _default_ws.setdefault(str(dev) + ":fused", Workspace())
+        workspace = _default_workspace(dev, "fused", stream)
     ws = workspace.get(need, dev)
     with_token_loss = with_token_loss or reduction == "none"
     if out is None:
@@ -330,7 +338,7 @@ def kd_forward_backward(hidden_s: torch.Tensor, weight_s: torch.Tensor, hidden_t
     if need == 0:
         raise ValueError("invalid KD problem shape")
     if workspace is None:
-        workspace = _default_ws.setdefault(str(dev) + ":kd", Workspace())
+        workspace = _default_workspace(dev, "kd", stream)
     ws = workspace.get(need, dev)
     out = {"loss": torch.empty(1, dtype=torch.float32, device=dev),
            "token_loss": torch.empty(N, dtype=torch.float32, device=dev),
@@ -361,7 +369,7 @@ def check_device_status(workspace: Optional[Workspace] = None, device=None, stre
         wss = [workspace]
     else:
         dev = str(device or torch.device("cuda", torch.cuda.current_device()))
-        wss = [w for k, w in _default_ws.items() if k == dev or k.startswith(dev + ":")]
+        wss = [w for k, w in _default_ws.items() if k.startswith(dev + ":") or k.startswith(dev + "@")]
     for ws in wss:
         if ws.buf is not None:
             check(lib.lce_check_device_status(_ptr(ws.buf), _stream(stream)), "lce_check_device_status")
@@ -416,7 +424,7 @@ class LinearCrossEntropyFusedFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, hidden, weight, labels, ignore_index, reduction, grad_scale):
         dev = hidden.device
-        ws = _default_ws.setdefault(str(dev) + ":fused", Workspace())
+        ws = _default_workspace(dev, "fused")
         g = torch.full((1,), float(grad_scale), dtype=torch.float32, device=dev)
         out = forward_backward(hidden, weight, labels, grad_loss=g, ignore_index=ignore_index, reduction=reduction,
                                workspace=ws)

@@ -277,6 +277,29 @@ def test_deterministic_rerun(cuda_lib):
     assert a["loss"] == b["loss"]
 
 
+def test_default_workspaces_are_per_stream(cuda_lib):
+    """Calls without an explicit workspace on two streams at once get separate
+    default scratch (a shared buffer would race): both results equal the
+    serial ones bitwise."""
+    import paper_2605_21442_b200 as F
+
+    a = small(3000, 256, 2000, seed=41)
+    b = small(2000, 256, 3000, seed=42)
+    ref_a = F.forward_backward(a.hidden, a.weight, a.labels)
+    ref_b = F.forward_backward(b.hidden, b.weight, b.labels)
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    with torch.cuda.stream(s1):
+        got_a = F.forward_backward(a.hidden, a.weight, a.labels)
+    with torch.cuda.stream(s2):
+        got_b = F.forward_backward(b.hidden, b.weight, b.labels)
+    torch.cuda.synchronize()
+    for ref, got in ((ref_a, got_a), (ref_b, got_b)):
+        for k in ("loss", "lse", "dhidden", "dweight"):
+            assert torch.equal(ref[k], got[k]), k
+    F.check_device_status()
+
+
 @pytest.mark.parametrize("lock", ["0", "1"])
 @pytest.mark.parametrize("path", ["fused", "split"])
 def test_k_lockstep_is_timing_only(cuda_lib, monkeypatch, lock, path):
