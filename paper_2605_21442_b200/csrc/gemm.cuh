@@ -108,12 +108,17 @@ struct LockSmem {
   uint32_t slowest;  // min over clusters of their published steps (monitor)
   uint32_t done;     // producer finished
 };
+// The producer and the monitor exchange these words with shared-memory
+// atomics (single writer per word, values only grow): no barrier between
+// them, and no plain racing accesses.
+__device__ __forceinline__ uint32_t lock_ld(uint32_t* p) { return atomicOr(p, 0u); }
+__device__ __forceinline__ void lock_st(uint32_t* p, uint32_t v) { atomicExch(p, v); }
 
-__device__ __forceinline__ void lockstep_gate(const GemmDims& d, volatile LockSmem* ls, uint32_t steps, bool& on) {
-  ls->steps = steps;
-  if (!on || steps <= ls->slowest + static_cast<uint32_t>(d.lock_d)) return;
+__device__ __forceinline__ void lockstep_gate(const GemmDims& d, LockSmem* ls, uint32_t steps, bool& on) {
+  lock_st(&ls->steps, steps);
+  if (!on || steps <= lock_ld(&ls->slowest) + static_cast<uint32_t>(d.lock_d)) return;
   const unsigned long long t0 = globaltimer_ns();
-  while (steps > ls->slowest + static_cast<uint32_t>(d.lock_d)) {
+  while (steps > lock_ld(&ls->slowest) + static_cast<uint32_t>(d.lock_d)) {
     if (globaltimer_ns() - t0 > kLockTimeoutNs) {  // a cluster is not running: stop waiting
       on = false;
       return;
@@ -122,15 +127,17 @@ __device__ __forceinline__ void lockstep_gate(const GemmDims& d, volatile LockSm
   }
 }
 
-__device__ __forceinline__ void lockstep_monitor(const GemmDims& d, volatile LockSmem* ls, int cluster,
-                                                 int nclusters, int lane) {
+__device__ __forceinline__ void lockstep_monitor(const GemmDims& d, LockSmem* ls, int cluster, int nclusters,
+                                                 int lane) {
   const unsigned long long tag = static_cast<unsigned long long>(d.lock_gen) << 32;
   for (;;) {
-    const uint32_t done = __shfl_sync(0xffffffffu, ls->done, 0);
-    const uint32_t mine = done ? 0xffffffffu : ls->steps;
-    if (lane == 0)
+    uint32_t done = 0, mine = 0;
+    if (lane == 0) {
+      done = lock_ld(&ls->done);
+      mine = done ? 0xffffffffu : lock_ld(&ls->steps);
       asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(d.lock_prog + cluster), "l"(tag | mine) : "memory");
-    if (done) return;
+    }
+    if (__shfl_sync(0xffffffffu, done, 0)) return;
     uint32_t mn = 0xffffffffu;
     for (int c = lane; c < nclusters; c += 32) {
       unsigned long long v;
@@ -139,7 +146,7 @@ __device__ __forceinline__ void lockstep_monitor(const GemmDims& d, volatile Loc
       mn = st < mn ? st : mn;
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
-    if (lane == 0) ls->slowest = mn;
+    if (lane == 0) lock_st(&ls->slowest, mn);
     __nanosleep(256);
   }
 }
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kPairStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile LockSmem* lsm = reinterpret_cast<volatile LockSmem*>(tmem_slot + 4);
+  LockSmem* lsm = reinterpret_cast<LockSmem*>(tmem_slot + 4);
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
@@ -506,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (lock) lsm->done = 1;
+      if (lock) lock_st(&lsm->done, 1u);
     }
   } else if (warp == 3) {
     if (lock) lockstep_monitor(dims, lsm, cluster, nclusters, lane);
@@ -620,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + kWideStages;  // [2]: accumulator half computed
   uint64_t* tempty = tfull + 2;           // [2]: accumulator half drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  volatile LockSmem* lsm = reinterpret_cast<volatile LockSmem*>(tmem_slot + 4);
+  LockSmem* lsm = reinterpret_cast<LockSmem*>(tmem_slot + 4);
   uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
 
   const int warp = threadIdx.x >> 5;
@@ -706,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (lock) lsm->done = 1;
+      if (lock) lock_st(&lsm->done, 1u);
     }
   } else if (warp == 3) {
     if (lock) lockstep_monitor(dims, lsm, cluster, nclusters, lane);
