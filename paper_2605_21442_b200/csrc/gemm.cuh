@@ -127,9 +127,16 @@ __device__ __forceinline__ void lockstep_gate(const GemmDims& d, LockSmem* ls, u
   }
 }
 
+#ifndef LCE_LOCK_MON
+#define LCE_LOCK_MON 1  // A/B: 0 = no monitor loop, 2 = publish only (no polling)
+#endif
+#ifndef LCE_LOCK_SLEEP
+#define LCE_LOCK_SLEEP 2000
+#endif
 __device__ __forceinline__ void lockstep_monitor(const GemmDims& d, LockSmem* ls, int cluster, int nclusters,
                                                  int lane) {
   const unsigned long long tag = static_cast<unsigned long long>(d.lock_gen) << 32;
+  if (LCE_LOCK_MON == 0) return;
   for (;;) {
     uint32_t done = 0, mine = 0;
     if (lane == 0) {
@@ -138,6 +145,10 @@ __device__ __forceinline__ void lockstep_monitor(const GemmDims& d, LockSmem* ls
       asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(d.lock_prog + cluster), "l"(tag | mine) : "memory");
     }
     if (__shfl_sync(0xffffffffu, done, 0)) return;
+    if (LCE_LOCK_MON == 2) {
+      __nanosleep(LCE_LOCK_SLEEP);
+      continue;
+    }
     uint32_t mn = 0xffffffffu;
     for (int c = lane; c < nclusters; c += 32) {
       unsigned long long v;
@@ -147,7 +158,7 @@ __device__ __forceinline__ void lockstep_monitor(const GemmDims& d, LockSmem* ls
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
     if (lane == 0) lock_st(&ls->slowest, mn);
-    __nanosleep(256);
+    __nanosleep(LCE_LOCK_SLEEP);
   }
 }
 

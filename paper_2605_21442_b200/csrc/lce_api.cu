@@ -543,26 +543,34 @@ int use_wide(int cls, int dflt) {
   return dflt;
 }
 
-// K-lockstep of the persistent wide-tile grids (gemm.cuh lockstep_gate /
+// K-lockstep of the persistent GEMM grids (gemm.cuh lockstep_gate /
 // lockstep_monitor): one progress word per cluster in a device-global array;
 // every launch gets a new generation tag, so words left by earlier launches
-// read as "not started" (a CUDA-graph replay reuses its captured tag: for the
-// first microsecond, until every monitor has published again, words left by
-// the previous replay read as "done" and gate nothing -- timing only).  Measured (one B200, in-step, medians of 4-5): the
-// fused step +1.3% at 8B and +4.7% at 70B (the dH / dW GEMMs' DRAM reads
-// drop from 12.6 / 13.9 to 6.2 / 6.7 GB per 8B chunk, cold-cache ncu); on
-// the short-K pair-tile GEMMs (1B dW: -17%) the gate's stalls cost more than
-// the traffic it saves, so it is on for wide tiles only.  LCE_LOCK[_<class>]
+// read as "not started" (a CUDA-graph replay reuses its captured tag: until
+// every monitor has published again, words left by the previous replay read
+// as "done" and gate nothing -- timing only).  Measured (one B200, in-step,
+// medians of 3-4, monitor polling every 2 us; DESIGN.md section 5 "Power"):
+// the dH / dW GEMMs' DRAM reads drop from 12.6 / 13.9 to 6.2 / 6.7 GB per 8B
+// chunk (cold-cache ncu); step +1.1-5.1% (8B fused), +6.2% (70B fused),
+// +0.4-2.5% (8B split) over no lockstep, the more the box is power-limited.
+// Short-K pair-tile launches (1B / packed-Qwen dH, dW; forward and G at
+// D < 4096) lose more to the gate's stalls than they save (1B pair dW -15%),
+// so they run without it.  LCE_LOCK[_<class>]
 // = 0 / 1 overrides, LCE_LOCK_D[_<class>] sets the allowed drift in k-block steps.
 __device__ unsigned long long g_lock_prog[128];
-constexpr int kLockD = 16;
+constexpr int kLockMinPairK = 4096;
+constexpr int kLockD = 16, kLockDPair = 32;  // k-blocks: 16 wide (1024-cycle) steps, 32 pair (512-cycle) steps
 void lockstep_config(GemmDims& d, int cls, bool wide) {
   static std::atomic<uint32_t> gen{0x5a5a0000u};
   char name[32];
   snprintf(name, sizeof(name), "LCE_LOCK_%d", cls);
   const char* env = getenv(name);
   if (!env) env = getenv("LCE_LOCK");
-  if (!(env ? atoi(env) != 0 : wide)) return;
+  // default: every wide-tile launch, and the pair-tile forward / G-recompute
+  // GEMMs when their K (= D) is long (>= 4096: 8B, 70B; the 1B / packed-Qwen
+  // heads measured -0.5 to -1.8%); never the short-K pair dH / dW launches
+  const bool dflt = wide || ((cls == LCE_K_FWD || cls == LCE_K_BWD_G) && !d.k_dev && d.k_static >= kLockMinPairK);
+  if (!(env ? atoi(env) != 0 : dflt)) return;
   void* p = nullptr;
   if (cudaGetSymbolAddress(&p, g_lock_prog) != cudaSuccess) {
     cudaGetLastError();
@@ -571,7 +579,7 @@ void lockstep_config(GemmDims& d, int cls, bool wide) {
   snprintf(name, sizeof(name), "LCE_LOCK_D_%d", cls);
   const char* de = getenv(name);
   if (!de) de = getenv("LCE_LOCK_D");
-  const int dd = de ? atoi(de) : kLockD;
+  const int dd = de ? atoi(de) : (wide ? kLockD : kLockDPair);
   d.lock_prog = static_cast<unsigned long long*>(p);
   d.lock_gen = ++gen;
   d.lock_d = dd < 0 ? 0 : dd;
