@@ -27,6 +27,11 @@ struct Header {
   int32_t tp_bad;     // token parallelism: out-of-range labels anywhere (all-reduced)
 };
 
+__device__ __forceinline__ uint16_t bf16_bits(float a) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(a);  // RNE
+  return *reinterpret_cast<const uint16_t*>(&h);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // RNE
   return *reinterpret_cast<uint32_t*>(&h);
@@ -538,66 +543,67 @@ struct EpiAdamW : EpiBase {
       prefetch_l2(p.exp_avg_sq + o + t.n0 + 32 * c);
     }
   }
-  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, const TileInfo& t) {
-    const int r = t.m0 + t.row;
-    const bool valid = r < t.M;
+  // Each warp owns 32 accumulator rows (one per lane, its TMEM lane quarter).
+  // Per 32-column chunk the lanes stage g = c * acc in shared memory (row per
+  // lane), then walk the 32 rows with one COLUMN per lane, so every load and
+  // store of theta / m / v / w is one coalesced 128-byte (64-byte for w) row
+  // segment per warp instruction instead of 32 half-used sectors.
+  static __device__ __forceinline__ void apply(const Params& p, uint32_t taddr, TileInfo& t) {
+    const int l = t.row & 31;
+    const int row0 = t.m0 + (t.row - l);  // first row of this warp's 32
     const float cs = p.hdr->c;
-    const int64_t rowoff = static_cast<int64_t>(r) * p.ld;
+    float* st = reinterpret_cast<float*>(t.smem);  // 32 x 32 fp32 (no TMA stores in this epilogue)
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       float x[32];
       load_chunk(taddr, c, t.zero_acc, x);
       const int cb = t.n0 + c * 32;
-      if (!valid || cb >= t.N) continue;
-      if (cb + 32 <= t.N) {
-        // whole chunk in range: issue all 24 loads before any arithmetic so
-        // the row's three 128-byte segments are in flight together
-        float4 th[8], m[8], s[8];
+      if (cb >= t.N) break;  // uniform across the warp
+      __syncwarp();          // the previous chunk's reads of st are done
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          th[v] = *reinterpret_cast<const float4*>(p.theta + rowoff + cb + 4 * v);
-          m[v] = *reinterpret_cast<const float4*>(p.exp_avg + rowoff + cb + 4 * v);
-          s[v] = *reinterpret_cast<const float4*>(p.exp_avg_sq + rowoff + cb + 4 * v);
+      for (int v = 0; v < 8; ++v)  // row l, 16-byte unit v at unit v ^ (l & 7): conflict-free both ways
+        *reinterpret_cast<float4*>(st + l * 32 + ((v ^ (l & 7)) * 4)) =
+            make_float4(cs * x[4 * v], cs * x[4 * v + 1], cs * x[4 * v + 2], cs * x[4 * v + 3]);
+      __syncwarp();
+      const int col = cb + l;
+      const int rows = (col < t.N) ? min(32, t.M - row0) : 0;
+      // 16 rows at a time: their 48 state loads are in flight together
+#pragma unroll 1
+      for (int r0 = 0; r0 < 32; r0 += kRowsInFlight) {
+        float th[kRowsInFlight], m[kRowsInFlight], v[kRowsInFlight];
+#pragma unroll
+        for (int i = 0; i < kRowsInFlight; ++i) {
+          if (r0 + i < rows) {
+            const int64_t o = static_cast<int64_t>(row0 + r0 + i) * p.ld + col;
+            th[i] = p.theta[o];
+            m[i] = p.exp_avg[o];
+            v[i] = p.exp_avg_sq[o];
+          }
         }
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          step4(p, cs, x + 4 * v, th[v], m[v], s[v]);
-          store4(p, rowoff + cb + 4 * v, th[v], m[v], s[v]);
-        }
-      } else {
-        for (int v = 0; v < 8 && cb + 4 * v < t.N; ++v) {
-          const int64_t o = rowoff + cb + 4 * v;
-          float4 th = *reinterpret_cast<const float4*>(p.theta + o);
-          float4 m = *reinterpret_cast<const float4*>(p.exp_avg + o);
-          float4 s = *reinterpret_cast<const float4*>(p.exp_avg_sq + o);
-          step4(p, cs, x + 4 * v, th, m, s);
-          store4(p, o, th, m, s);
+        for (int i = 0; i < kRowsInFlight; ++i) {
+          const int r = r0 + i;
+          if (r < rows) {
+            const float g = st[r * 32 + ((((l >> 2) ^ (r & 7)) << 2) | (l & 3))];
+            step1(p, g, th[i], m[i], v[i]);
+            const int64_t o = static_cast<int64_t>(row0 + r) * p.ld + col;
+            p.theta[o] = th[i];
+            p.exp_avg[o] = m[i];
+            p.exp_avg_sq[o] = v[i];
+            p.w[o] = bf16_bits(th[i]);
+          }
         }
       }
     }
   }
-  // torch.optim.AdamW's single-tensor update order (R22) on 4 elements
-  static __device__ __forceinline__ void step4(const Params& p, float cs, const float* x, float4& th, float4& m,
-                                               float4& s) {
-    float* thv = &th.x;
-    float* mv = &m.x;
-    float* sv = &s.x;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float g = cs * x[e];
-      thv[e] = thv[e] * p.decay;
-      mv[e] = mv[e] + (1.f - p.beta1) * (g - mv[e]);  // torch: exp_avg.lerp_(grad, 1 - beta1)
-      sv[e] = p.beta2 * sv[e] + (1.f - p.beta2) * g * g;
-      const float denom = __fdiv_rn(__fsqrt_rn(sv[e]), p.sqrt_bc2) + p.eps;
-      thv[e] = thv[e] - p.step_size * __fdiv_rn(mv[e], denom);
-    }
-  }
-  static __device__ __forceinline__ void store4(const Params& p, int64_t o, const float4& th, const float4& m,
-                                                const float4& s) {
-    *reinterpret_cast<float4*>(p.theta + o) = th;
-    *reinterpret_cast<float4*>(p.exp_avg + o) = m;
-    *reinterpret_cast<float4*>(p.exp_avg_sq + o) = s;
-    *reinterpret_cast<uint2*>(p.w + o) = make_uint2(pack_bf16x2(th.x, th.y), pack_bf16x2(th.z, th.w));
+  static constexpr int kRowsInFlight = 32;
+  // torch.optim.AdamW's single-tensor update order (R22) on one element (g = c * dW)
+  static __device__ __forceinline__ void step1(const Params& p, float g, float& th, float& m, float& v) {
+    th = th * p.decay;
+    m = m + (1.f - p.beta1) * (g - m);  // torch: exp_avg.lerp_(grad, 1 - beta1)
+    v = p.beta2 * v + (1.f - p.beta2) * g * g;
+    const float denom = __fdiv_rn(__fsqrt_rn(v), p.sqrt_bc2) + p.eps;
+    th = th - p.step_size * __fdiv_rn(m, denom);
   }
 };
 
