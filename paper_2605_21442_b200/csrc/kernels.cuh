@@ -773,14 +773,17 @@ __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict_
   const int b = blockIdx.x;
   const int nv = hdr->n_valid;
   const int nvec = static_cast<int>(D / 8);
-  uint4* dst = reinterpret_cast<uint4*>(Hc + static_cast<int64_t>(b) * D);
+  // Hc == null (fused path: per-chunk H_c, gather_chunk_kernel): no copy,
+  // only the per-row gathers and the zero rows of dhidden
+  uint4* dst = Hc ? reinterpret_cast<uint4*>(Hc + static_cast<int64_t>(b) * D) : nullptr;
   if (b < nv) {
     const int src_row = idx[b];
     const uint4* src = reinterpret_cast<const uint4*>(H + static_cast<int64_t>(src_row) * D);
-    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
+    if (dst)
+      for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
     if (lse_in && threadIdx.x == 0) lse_c[b] = lse_in[src_row];
     if (grad_in && threadIdx.x == 0) grad_c[b] = grad_in[src_row];
-  } else if (b < ((nv + 255) & ~255)) {  // up to the 256-row pair tile: no stale row enters a GEMM
+  } else if (dst && b < ((nv + 255) & ~255)) {  // up to the 256-row pair tile: no stale row enters a GEMM
     for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
   }
   if (dhidden && b < N) {
@@ -790,6 +793,26 @@ __global__ void __launch_bounds__(128) gather_kernel(const uint16_t* __restrict_
       uint4* o = reinterpret_cast<uint4*>(dhidden + static_cast<int64_t>(b) * D);
       for (int v = threadIdx.x; v < nvec; v += blockDim.x) o[v] = make_uint4(0, 0, 0, 0);
     }
+  }
+}
+
+// Fused path: the compacted rows of one row chunk, [r0, r0 + cap), into a
+// chunk-sized H_c (one CTA per chunk row): rows < M = clamp(N_v - r0, 0, cap)
+// are hidden[idx[r0 + b]], rows [M, ceil256(M)) are zeroed (the GEMMs' last
+// pair tile reads them; zero rows keep every logit finite).  The whole-batch
+// H_c (2 N_v D bytes: 4.3 GB at 1M tokens of the 1B head) is never built.
+__global__ void __launch_bounds__(128) gather_chunk_kernel(const uint16_t* __restrict__ H, int64_t D,
+                                                           const int32_t* __restrict__ idx, const Header* hdr,
+                                                           int row_off, int cap, uint16_t* __restrict__ Hc) {
+  const int b = blockIdx.x;
+  const int M = min(max(hdr->n_valid - row_off, 0), cap);
+  const int nvec = static_cast<int>(D / 8);
+  uint4* dst = reinterpret_cast<uint4*>(Hc + static_cast<int64_t>(b) * D);
+  if (b < M) {
+    const uint4* src = reinterpret_cast<const uint4*>(H + static_cast<int64_t>(idx[row_off + b]) * D);
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = __ldg(src + v);
+  } else if (b < ((M + 255) & ~255)) {
+    for (int v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = make_uint4(0, 0, 0, 0);
   }
 }
 
@@ -1191,7 +1214,10 @@ __global__ void __launch_bounds__(256) reduce_dh_kernel(const float* __restrict_
 // The per-row reference of the stored probabilities: ref_i = h_i . w_{y_i} in
 // fp32 (the target logit up to summation order; any value within kScaledQMax
 // of the row's logits would do).  One warp per compact row; rows >= N_v get 0.
+// rowmap != null: row r of the compacted rows is row rowmap[r] of hc (= the
+// caller's hidden: the fused path keeps only a chunk-sized H_c).
 __global__ void __launch_bounds__(256) target_dot_kernel(const uint16_t* __restrict__ hc,
+                                                         const int32_t* __restrict__ rowmap,
                                                          const uint16_t* __restrict__ W, int64_t D,
                                                          const int32_t* __restrict__ yc, int32_t label_off,
                                                          int32_t n_cols, const Header* hdr, int rows,
@@ -1204,7 +1230,7 @@ __global__ void __launch_bounds__(256) target_dot_kernel(const uint16_t* __restr
     if (lane == 0) q_ref[r] = 0.f;
     return;
   }
-  const uint4* a = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(r) * D);
+  const uint4* a = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(rowmap ? rowmap[r] : r) * D);
   const uint4* b = reinterpret_cast<const uint4*>(W + static_cast<int64_t>(col) * D);
   float acc = 0.f;
   for (int v = lane; v < D / 8; v += 32) {
@@ -1234,7 +1260,8 @@ __global__ void __launch_bounds__(256) target_dot_kernel(const uint16_t* __restr
 // Rows in [M, Nc) get zero coefficients and zero Hs rows.  Block 0 also sets
 // the row extent of the conditional redo GEMM (N_v if flagged, else 0).
 __global__ void __launch_bounds__(256) scaled_prep_kernel(uint16_t* __restrict__ Q, int64_t ldq, int row_off,
-                                                          int cap, const uint16_t* __restrict__ hc, int64_t D,
+                                                          int cap, const uint16_t* __restrict__ hc,
+                                                          const int32_t* __restrict__ rowmap, int64_t D,
                                                           const int32_t* __restrict__ yc, int32_t label_off,
                                                           int32_t n_cols, const float* __restrict__ lse_c,
                                                           const float* __restrict__ zt,
@@ -1254,7 +1281,7 @@ __global__ void __launch_bounds__(256) scaled_prep_kernel(uint16_t* __restrict__
     return;
   }
   const int r = row_off + m;
-  const uint4* h = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(r) * D);
+  const uint4* h = reinterpret_cast<const uint4*>(hc + static_cast<int64_t>(rowmap ? rowmap[r] : r) * D);
   if (fallback) {
     if (threadIdx.x == 0) coef[m] = 1.f;
     for (int v = threadIdx.x; v < D / 8; v += blockDim.x) hs[v] = h[v];

@@ -137,8 +137,12 @@ struct FusedPlan {
   size_t hdr, idx, yc, zt, lsec, gsc, ltok, hc, pm, ps, z, g, slab;
   size_t vmloc, vmglob, vsz, vdh;  // vocab-parallel chunk exchange buffers
   size_t qref, coef, hs, qflag;    // scaled-q mode (R25): per-row reference, dH row factors, scaled H chunk, flags
+  bool chunk_hc;                   // CE fused path: H_c holds one row chunk (gathered per chunk), not the batch
   size_t total;
 };
+
+// LCE_FUSED_SCALED=0 selects the fused path's tile-max fix-up form (R24).
+bool fused_scaled_env() { return !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0); }
 
 int use_pair_units(int sms);
 int use_wide(int cls, int dflt);
@@ -227,7 +231,10 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   q.lsec = take(q.cap * 4);
   q.gsc = take(q.cap * 4);
   q.ltok = take(q.cap * 4);
-  q.hc = take(static_cast<size_t>((q.n_chunks * q.Nc) * q.D * 2));
+  // the CE fused path gathers one row chunk of H at a time (gather_chunk_kernel);
+  // KD keeps the batch's compacted rows
+  q.chunk_hc = !kd;
+  q.hc = take(static_cast<size_t>((q.chunk_hc ? 1 : q.n_chunks) * q.Nc * q.D * 2));
   q.pm = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
   q.ps = take(static_cast<size_t>(q.n_tiles * q.Nc * 4));
   q.z = kd ? take(static_cast<size_t>(q.Nc * q.ldv * 4)) : 0;
@@ -1520,12 +1527,17 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   LCE_TRY(tp_sync(tp, hdr, grad_loss, p->reduction, s));
   {
     LaunchScope sc(LCE_K_GATHER, s);
-    gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden, fp.D, N, idx, hdr, hc, nullptr, nullptr,
+    // per-row gathers and the zero dhidden rows of ignored tokens; the rows of
+    // H themselves are gathered chunk by chunk below
+    gather_kernel<<<static_cast<unsigned>(fp.cap), 128, 0, s>>>(hidden, fp.D, N, idx, hdr, nullptr, nullptr, nullptr,
                                                                row_grad, gsc, labels, p->ignore_index,
                                                                p->vocab_total, dhidden);
     LCE_TRY(last_error());
   }
   const int32_t Nc = static_cast<int32_t>(fp.Nc), Vl = static_cast<int32_t>(fp.Vl), D = static_cast<int32_t>(fp.D);
+  CUtensorMap t_h_k, t_h_mn;  // the chunk's H_c rows (one chunk-sized buffer, refilled per chunk)
+  LCE_TRY(map_kmajor(&t_h_k, hc, fp.Nc, fp.D, fp.D, BM));
+  LCE_TRY(map_mnmajor(&t_h_mn, hc, fp.Nc, fp.D, fp.D));
   CUtensorMap t_w_k, t_w_mn, t_g_k, t_g_mn;
   LCE_TRY(map_kmajor(&t_w_k, weight, fp.Vl, fp.D, fp.D, b_box_rows()));
   LCE_TRY(map_mnmajor(&t_w_mn, weight, fp.Vl, fp.D, fp.D));
@@ -1537,7 +1549,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   // with out-of-range rows redo their forward in the tile-max form on the GPU
   // (no host sync; under vocab parallelism each rank decides for its own
   // partials).  LCE_FUSED_SCALED=0 selects the fix-up form.
-  const bool scaled = !(getenv("LCE_FUSED_SCALED") && atoi(getenv("LCE_FUSED_SCALED")) == 0);
+  const bool scaled = fused_scaled_env();
   float* qref = reinterpret_cast<float*>(ws + fp.qref);
   float* coef = reinterpret_cast<float*>(ws + fp.coef);
   uint16_t* hs = reinterpret_cast<uint16_t*>(ws + fp.hs);
@@ -1549,7 +1561,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
     LaunchScope sc(LCE_K_GATHER, s);
     const int rows = static_cast<int>(fp.n_chunks * fp.Nc);
     target_dot_kernel<<<static_cast<unsigned>((rows + 7) / 8), 256, 0, s>>>(
-        hc, weight, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, hdr, rows, qref);
+        hidden, idx, weight, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, hdr, rows, qref);
     LCE_TRY(last_error());
   }
   // vocab-parallel: the target row of W lives on one rank (the others add 0)
@@ -1559,10 +1571,11 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
   LCE_TRY(nst);
   for (int64_t q = 0; q < fp.n_chunks; ++q) {
     const int32_t r0 = static_cast<int32_t>(q * fp.Nc);
-    const uint16_t* hq = hc + static_cast<int64_t>(r0) * fp.D;
-    CUtensorMap t_h_k, t_h_mn;
-    LCE_TRY(map_kmajor(&t_h_k, hq, fp.Nc, fp.D, fp.D, BM));
-    LCE_TRY(map_mnmajor(&t_h_mn, hq, fp.Nc, fp.D, fp.D));
+    {  // S0 for the chunk: its compacted rows of H into the chunk-sized H_c
+      LaunchScope sc(LCE_K_GATHER, s);
+      gather_chunk_kernel<<<static_cast<unsigned>(fp.Nc), 128, 0, s>>>(hidden, fp.D, idx, hdr, r0, Nc, hc);
+      LCE_TRY(last_error());
+    }
     if (scaled) LCE_CUDA(cudaMemsetAsync(qflag, 0, sizeof(int32_t), s));
     // S1+S2 (+ keep q of the chunk in bf16): z = H_q W^T, LSE partials
     {
@@ -1610,7 +1623,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
       {
         LaunchScope sc(LCE_K_BWD_G, s);
         scaled_prep_kernel<<<static_cast<unsigned>(fp.Nc), 256, 0, s>>>(
-            G, fp.ldv, r0, Nc, hc, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, lsec, zt, qref,
+            G, fp.ldv, r0, Nc, hidden, idx, fp.D, yc, static_cast<int32_t>(p->vocab_start), Vl, lsec, zt, qref,
             row_grad ? gsc : nullptr, hdr, qflag, redo_rows, coef, hs);
         LCE_TRY(last_error());
       }
