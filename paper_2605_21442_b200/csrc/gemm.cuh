@@ -97,7 +97,9 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 //     ahead of the slowest cluster as last seen by the monitor;
 //   * the monitor (warp 3, otherwise idle; lockstep_monitor) publishes this
 //     cluster's count to lock_prog[cluster] and polls every cluster's count
-//     (one load per lane) about once a microsecond until the producer is done.
+//     (one load per lane) about every 2 us until the producer is done (a
+//     256-ns poll made the five progress lines an L2 hot spot that delayed
+//     the operand loads hashed to the same slices: pair forward -26%).
 // A cluster that is not running makes the gate time out, after which that
 // producer stops waiting for the rest of the launch: the lockstep can delay a
 // producer, never block it.  The peer CTA's producer is paced by the shared
