@@ -160,7 +160,11 @@ __device__ __forceinline__ void lockstep_monitor(const GemmDims& d, LockSmem* ls
     }
     mn = __reduce_min_sync(0xffffffffu, mn);
     if (lane == 0) lock_st(&ls->slowest, mn);
-    __nanosleep(LCE_LOCK_SLEEP);
+    // wait out the poll period in short naps, leaving as soon as the producer is done
+    for (int i = 0; i < LCE_LOCK_SLEEP / 250; ++i) {
+      if (__shfl_sync(0xffffffffu, lane == 0 ? lock_ld(&ls->done) : 0u, 0)) break;
+      __nanosleep(250);
+    }
   }
 }
 
@@ -460,8 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
   const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
-  // K-lockstep: gate in the leader's producer, monitor in its warp 3
-  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0;
+  // K-lockstep: gate in the leader's producer, monitor in its warp 3 (nothing to pace in an empty launch)
+  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0 && num_tiles > 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -659,8 +663,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int S = dims.ksplit > 1 ? dims.ksplit : 1;
   const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
   const int num_tiles = num_m * num_n * S;
-  // K-lockstep: gate in the leader's producer, monitor in its warp 3
-  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0;
+  // K-lockstep: gate in the leader's producer, monitor in its warp 3 (nothing to pace in an empty launch)
+  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0 && num_tiles > 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
