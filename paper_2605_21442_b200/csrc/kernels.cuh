@@ -350,6 +350,33 @@ struct EpiDH : EpiBase {
       }
       return;
     }
+    if (p.part && p.use_map) {  // split-K partial through TMA stores (map over [split * rows, ld] slabs)
+      const int l = t.row & 31;
+      const float rc = (p.row_coef && valid) ? p.row_coef[r] : 1.f;
+      const int slab_rows = static_cast<int>(p.part_stride / p.ld);
+      // a warp's 32-row box past the slab's rows (a wide tile taller than the
+      // chunk) would land in the next slab: skip it (uniform across the warp)
+      if (t.m0 + (t.row - l) >= slab_rows) return;
+      const int grow = t.split * slab_rows + t.m0 + (t.row - l);
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float x[32];
+        load_chunk(taddr, c, t.zero_acc, x);
+        if (t.n0 + c * 32 >= t.N) continue;  // uniform across the warp
+        uint8_t* st = stage_next(t);
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4*>(st + l * 128 + ((v ^ (l & 7)) * 16)) =
+              make_float4(rc * x[4 * v], rc * x[4 * v + 1], rc * x[4 * v + 2], rc * x[4 * v + 3]);
+        fence_async_smem();
+        __syncwarp();
+        if (l == 0) {
+          tma_store_2d_hint(&p.map, st, t.n0 + c * 32, grow, t.st_policy);
+          tma_store_commit();
+        }
+      }
+      return;
+    }
     if (p.part) {  // split-K partial: plain fp32 store, no read-modify-write
       float* prow = p.part + t.split * p.part_stride + static_cast<int64_t>(r) * p.ld;
       const float rc = (p.row_coef && valid) ? p.row_coef[r] : 1.f;  // linear: each slab scaled

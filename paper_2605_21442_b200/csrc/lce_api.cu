@@ -1399,6 +1399,11 @@ lce_status_t chunk_grads(const FusedPlan& fp, lce_comm_t comm, int sms, cudaStre
     float* part = split > 1 ? slab : (comm ? vdh : nullptr);
     EpiDH::Params ep{nullptr, fp.D, 1, 1, hdr, dhidden, idx, r0, 0, part, fp.Nc * fp.D};
     ep.row_coef = row_coef;
+    // split-K slabs through TMA stores (LCE_DH_SLAB_TMA=0: per-row 16-byte stores)
+    if (part && !(getenv("LCE_DH_SLAB_TMA") && atoi(getenv("LCE_DH_SLAB_TMA")) == 0)) {
+      ep.use_map = 1;
+      LCE_TRY(map_f32_store(&ep.map, part, fp.D, (split > 1 ? split : 1) * fp.Nc, fp.D));
+    }
     LCE_TRY((launch_gemm<false, true, EpiDH>(LCE_K_BWD_DH, t_g_k, t_w_mn, d, ep, sms, s, fp.wide_dh)));
   }
   if (split > 1) {
