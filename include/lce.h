@@ -122,8 +122,10 @@ typedef struct {
                                  lce_backward: 32768 vocab columns of bf16 G
                                  (2 * ceil256(N) * 32768 bytes) clamped to
                                  [512 MiB, 4 GiB] and never below 4096 columns;
-                                 lce_forward_backward: 2 GiB of bf16 q/G rows;
-                                 KD: 4 GiB.  A performance knob only.            */
+                                 lce_forward_backward: 2 GiB of bf16 q/G rows,
+                                 or ceil(N/2) rows (two chunks) when those
+                                 take at most 4 GiB; KD: 4 GiB.  A
+                                 performance knob only.                          */
 } lce_problem_t;
 
 /* Bytes of caller-provided device workspace both lce_forward and lce_backward
@@ -216,7 +218,8 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm,
  * NULL = 1; lce_expect_grad checks an autograd caller's actual one later).
  * dW is accumulated across row chunks in fp32 (dweight_flags: 0 or
  * LCE_DW_ACCUMULATE; LCE_DW_BF16 -> LCE_ERR_ARG).  Nc is set by
- * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB) and is at
+ * chunk_budget_bytes (bytes of the bf16 chunk buffer; 0 = 2 GiB, raised to
+ * ceil(N/2) rows when those take at most 4 GiB) and is at
  * most half the rows, so the buffer never holds all N x V_l probabilities.
  * With a vocab-parallel comm each row chunk's (max, sum-exp, target
  * logit) are combined with the same MAX / SUM all-reduces as lce_forward, and

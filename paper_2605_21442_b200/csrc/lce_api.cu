@@ -117,6 +117,7 @@ bool make_plan(const lce_problem_t* p, Plan* pl) {
 // path keeps fp32 logits for student and teacher (see KdPlan).
 constexpr int64_t kDefaultFusedBudget = 2ll << 30;
 constexpr int64_t kDefaultKdBudget = 4ll << 30;
+constexpr int64_t kTwoChunkBudget = 4ll << 30;
 // Workspace sizes are host-pure, so the plan assumes a full B200 (148 SMs) when
 // it reserves the dH split-K slabs; at launch the split factor and tile shape
 // are re-derived from the current device's SM count (fit_plan_to_device),
@@ -199,7 +200,18 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
   q.ldv = round_up(q.Vl, BN);
   q.n_tiles = ceil_div(q.Vl, BN);
   const int64_t per_elem = kd ? 6 : 2;
-  const int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
+  int64_t budget = p->chunk_budget_bytes > 0 ? p->chunk_budget_bytes : kDefaultFusedBudget;
+  // Default for CE: the fewest chunks the two-chunk rule allows (N_c = N / 2)
+  // while such a chunk stays <= kTwoChunkBudget.  Every non-empty chunk pays a
+  // full pass over W in the forward and dH GEMMs and a full fp32 pass over dW
+  // (store, then reduce-adds), whatever its row count; with padded batches the
+  // valid rows (compacted first) then often fit one chunk (packed Qwen: N_v =
+  // 7,177 of 16,384 rows: 5,632 + 1,545-row chunks at 2 GiB, one 8,192-row
+  // chunk here, 20.6 -> 18.7 ms per step, +1.5 GB; profiles/round2c_budget.log)
+  if (!kd && p->chunk_budget_bytes <= 0) {
+    const int64_t half = per_elem * q.ldv * round_up(ceil_div(q.cap, 2), kPairBM);
+    if (half > budget && half <= kTwoChunkBudget) budget = half;
+  }
   int64_t nc_max = (budget / (per_elem * q.ldv)) / kPairBM * kPairBM;
   if (nc_max < kPairBM) nc_max = kPairBM;
   if (nc_max > q.cap) nc_max = q.cap;
