@@ -76,6 +76,23 @@ def test_fused_workspace_never_holds_all_logits(L):
             assert 0 < w < N * V * 2, (N, D, V, budget, w)
 
 
+def test_fused_default_budget_prefers_two_chunks(L):
+    """The fused default chunk is the two-chunk size ceil(N/2) when that bf16
+    chunk takes <= 4 GiB (packed Qwen: one chunk then holds every valid row),
+    else 2 GiB (70B); the plan is host-pure, so the workspace shows it."""
+    def ws(N, D, V, budget=0):
+        return L.lib.lce_fused_workspace_bytes(ctypes.byref(prob(L, N, D, V, budget=budget)))
+
+    ldv = lambda V: (V + 255) // 256 * 256  # noqa: E731
+    # packed Qwen: 2 GiB would give 5,632-row chunks; the default is 8,192 rows
+    assert ws(16384, 3584, 152064) == ws(16384, 3584, 152064, budget=2 * ldv(152064) * 8192)
+    assert ws(16384, 3584, 152064) > ws(16384, 3584, 152064, budget=2 << 30)
+    # 70B: the 32,768-row half chunk (8.4 GB) is over 4 GiB: the 2 GiB default stays
+    assert ws(65536, 8192, 128256) == ws(65536, 8192, 128256, budget=2 << 30)
+    # 8B: 2 GiB already gives two chunks
+    assert ws(16384, 4096, 128256) == ws(16384, 4096, 128256, budget=2 << 30)
+
+
 @pytest.mark.parametrize("bad", [
     dict(N=-1), dict(D=0), dict(D=12), dict(V=0), dict(vl=10, vstart=128250), dict(N=1 << 31),
 ])
