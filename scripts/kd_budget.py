@@ -9,7 +9,7 @@ from synth.inputs import make_config, make_inputs
 inp = make_config("llama8b", device="cuda")
 H, W, y = inp.hidden, inp.weight, inp.labels
 t = make_inputs(H.shape[0], H.shape[1], W.shape[0], k=12, device="cuda", label_override=y.cpu().numpy())
-for b in (0, 6 << 30, 8 << 30, 11 << 30):
+for b in (0, 6 << 30, 8 << 30, 11 << 30, 0, 11 << 30):
     ws = F.Workspace()
     f = lambda: F.kd_forward_backward(H, W, t.hidden, t.weight, y, workspace=ws, chunk_budget_bytes=b)
     for _ in range(2): f()

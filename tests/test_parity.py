@@ -860,6 +860,21 @@ def test_fused_many_row_chunks_with_packed_labels(cuda_lib, variant):
     assert fro_rel(g["dW"], one["dW"]) <= 1e-5
 
 
+@pytest.mark.parametrize("n_valid", [511, 512, 513, 1024])
+def test_fused_default_plan_chunk_boundary(cuda_lib, n_valid):
+    """Default (two-chunk) plan, N = 1024 -> 512-row chunks: the compacted
+    valid rows end just before, at and just after the chunk boundary (the
+    second chunk empty, or holding one row) and fill both chunks."""
+    N, D, V = 1024, 128, 3000
+    rng = np.random.default_rng(n_valid)
+    lab = rng.integers(0, V, N).astype(np.int32)
+    lab[rng.permutation(N)[:N - n_valid]] = IGNORE
+    inp = small(N, D, V, seed=n_valid, labels=lab)
+    g = fused_run(inp)
+    assert g["n_valid"] == n_valid
+    assert_parity(g, oracle_run(inp), lab)
+
+
 def test_fused_none_accumulate_and_empty(cuda_lib):
     inp = small(300, 64, 1000, seed=11)
     gvec = np.linspace(-2, 1, 300)
