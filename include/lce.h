@@ -315,6 +315,13 @@ int lce_abi_version(void);
 /* Total number of CUDA kernels this library has launched since load. */
 uint64_t lce_launch_count(void);
 
+/* NVTX: every lce_forward / lce_backward / lce_backward_adamw /
+ * lce_forward_backward / lce_kd_forward_backward call is an NVTX range of
+ * that name, and every kernel launch inside it a nested range named by its
+ * step (the class names below: "S1+S2 forward GEMM + LSE", "S5 dW GEMM", ...).
+ * Header-only NVTX3: free unless a tool is attached (e.g. ncu --nvtx
+ * --nvtx-include "lce_forward_backward/").                                  */
+
 /* Kernel classes for the profiler below. */
 typedef enum {
   LCE_K_PREP = 0,     /* S0 label scan + stable compaction          */

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <sys/syscall.h>
 #include <unistd.h>
 #include <stdio.h>
@@ -461,12 +462,26 @@ struct Profiler {
   }
 } g_prof;
 
+// NVTX (header-only NVTX3; a no-op unless a tool such as nsys or ncu
+// --nvtx is attached): one range per API call (NvtxCall) and one per kernel
+// launch named by its step class (LaunchScope), so a timeline shows S0-S7.
+constexpr const char* kClassName[LCE_K_COUNT] = {"S0 prep",         "S0 gather", "S1+S2 forward GEMM + LSE",
+                                                 "S3 combine",      "S4 G",      "S6 dH GEMM",
+                                                 "S5 dW GEMM",      "S7 dH finalize", "NCCL"};
+struct NvtxCall {
+  explicit NvtxCall(const char* name) { nvtxRangePushA(name); }
+  ~NvtxCall() { nvtxRangePop(); }
+  NvtxCall(const NvtxCall&) = delete;
+  NvtxCall& operator=(const NvtxCall&) = delete;
+};
+
 struct LaunchScope {
   int cls;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
   int slot = -1;
-  LaunchScope(int c, cudaStream_t st) : cls(c), s(st) {
+  NvtxCall range;
+  LaunchScope(int c, cudaStream_t st) : cls(c), s(st), range(kClassName[c]) {
     if (g_prof.on) {
       a = g_prof.get();
       b = g_prof.get();
@@ -1092,6 +1107,7 @@ size_t lce_workspace_bytes(const lce_problem_t* p) {
 lce_status_t lce_forward(const lce_problem_t* p, lce_comm_t comm_in, const uint16_t* hidden, const uint16_t* weight,
                          const int32_t* labels, float* loss, float* lse, float* token_loss, int32_t* n_valid,
                          void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxCall nvtx_call("lce_forward");
   Plan pl;
   LCE_TRY(validate(p, comm_in, workspace_bytes, workspace, &pl));
   lce_comm_t comm = vocab_comm(comm_in), tp = token_comm(comm_in);
@@ -1461,6 +1477,7 @@ lce_status_t lce_backward(const lce_problem_t* p, lce_comm_t comm, const uint16_
                           const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
                           void* dweight, int dweight_flags, void* workspace, size_t workspace_bytes,
                           void* stream) {
+  NvtxCall nvtx_call("lce_backward");
   return backward_impl(p, comm, hidden, weight, labels, lse, grad_loss, dhidden, dweight, dweight_flags, nullptr,
                        workspace, workspace_bytes, stream);
 }
@@ -1469,6 +1486,7 @@ lce_status_t lce_backward_adamw(const lce_problem_t* p, lce_comm_t comm, const u
                                 const int32_t* labels, const float* lse, const float* grad_loss, uint16_t* dhidden,
                                 float* master_weight, float* exp_avg, float* exp_avg_sq, const lce_adamw_t* hp,
                                 void* workspace, size_t workspace_bytes, void* stream) {
+  NvtxCall nvtx_call("lce_backward_adamw");
   if (!hp || !master_weight || !exp_avg || !exp_avg_sq || !weight) return LCE_ERR_NULL;
   if (hp->step < 1 || !(hp->beta1 >= 0.f && hp->beta1 < 1.f) || !(hp->beta2 >= 0.f && hp->beta2 < 1.f) ||
       !(hp->eps > 0.f) || !(hp->lr >= 0.f) || !(hp->weight_decay >= 0.f))
@@ -1490,6 +1508,7 @@ lce_status_t lce_forward_backward(const lce_problem_t* p, lce_comm_t comm_in, co
                                   float* loss, float* lse, float* token_loss, int32_t* n_valid, uint16_t* dhidden,
                                   float* dweight, int dweight_flags, void* workspace, size_t workspace_bytes,
                                   void* stream) {
+  NvtxCall nvtx_call("lce_forward_backward");
   if (!p) return LCE_ERR_NULL;
   if (dweight_flags & ~LCE_DW_ACCUMULATE) return LCE_ERR_ARG;  // fp32 only: dW is summed over row chunks
   const bool accumulate_dweight = dweight_flags != 0;
@@ -1684,6 +1703,7 @@ lce_status_t lce_kd_forward_backward(const lce_problem_t* p, lce_comm_t comm_in,
                                      float* loss, float* token_loss, int32_t* n_valid, uint16_t* dhidden_s,
                                      float* dweight_s, int dweight_flags, void* workspace,
                                      size_t workspace_bytes, void* stream) {
+  NvtxCall nvtx_call("lce_kd_forward_backward");
   if (!p) return LCE_ERR_NULL;
   if (dweight_flags & ~LCE_DW_ACCUMULATE) return LCE_ERR_ARG;  // fp32 only: dW is summed over row chunks
   const bool accumulate_dweight = dweight_flags != 0;
