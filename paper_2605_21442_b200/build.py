@@ -20,6 +20,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblce.so")
+# same sources with -DLCE_DEBUG_SYNC: every device spin wait traps after 2 s
+# (sm100.cuh SpinGuard); hang detection where compute-sanitizer is unavailable
+DEBUG_LIB = os.path.join(PKG, "liblce_debug.so")
 SOURCES = [os.path.join(CSRC, "lce_api.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("sm100.cuh", "gemm.cuh", "kernels.cuh")] + [
     os.path.join(ROOT, "include", "lce.h")
@@ -82,5 +85,15 @@ def build(force: bool = False, verbose: bool = False, dest: str = LIB, defines: 
     return dest
 
 
+def build_debug(force: bool = False) -> str:
+    """liblce_debug.so (LCE_LIB_PATH=... loads it instead of liblce.so)."""
+    if not force and os.path.exists(DEBUG_LIB) and all(os.path.getmtime(d) <= os.path.getmtime(DEBUG_LIB)
+                                                       for d in DEPS):
+        return DEBUG_LIB
+    return build(force=True, dest=DEBUG_LIB, defines=("LCE_DEBUG_SYNC",))
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose="--verbose" in sys.argv))
+    if "--debug" in sys.argv:
+        print(build_debug(force=True))

@@ -776,8 +776,8 @@ __global__ void nvls_barrier_kernel(uint32_t* mc_flag, const uint32_t* uc_flag, 
     atomicAdd(mc_flag, 1u);
   else
     multimem_red_release_add_u32(mc_flag, 1u);
-  while (ld_acquire_sys_u32(uc_flag) < target) {
-  }
+  SpinGuard g;
+  while (ld_acquire_sys_u32(uc_flag) < target) g.tick("NVLS flag", target, 0);
 }
 
 // lce_expect_grad: the upstream gradient the fused call assumed vs the actual one.

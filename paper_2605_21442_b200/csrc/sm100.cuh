@@ -10,6 +10,9 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#ifdef LCE_DEBUG_SYNC
+#include <cstdio>
+#endif
 
 namespace lce {
 
@@ -54,11 +57,42 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t bar, uint32_t parity)
 }
 
 
+// Debug builds (-DLCE_DEBUG_SYNC, liblce_debug.so): every spin wait that has
+// not completed after LCE_DEBUG_SYNC_NS of %globaltimer (default 2 s; the
+// longest legitimate wait is one work item, about a millisecond) prints what
+// it waited on and traps, so a lost arrive or a wrong phase parity surfaces as
+// a launch error instead of a hang.  Release builds compile the guard away.
+#ifdef LCE_DEBUG_SYNC
+#ifndef LCE_DEBUG_SYNC_NS
+#define LCE_DEBUG_SYNC_NS 2000000000ull
+#endif
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  uint32_t n = 0;
+  __device__ __forceinline__ void tick(const char* what, uint32_t addr, uint32_t parity) {
+    if ((++n & 1023u) != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t0 == 0) {
+      t0 = t;
+    } else if (t - t0 > LCE_DEBUG_SYNC_NS) {
+      printf("lce debug: %s wait timed out (0x%x, parity %u) in block %d thread %d\n", what, addr, parity,
+             blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+};
+#else
+struct SpinGuard {
+  __device__ __forceinline__ void tick(const char*, uint32_t, uint32_t) {}
+};
+#endif
+
 // Blocks until the phase with the given parity has completed.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  while (!mbar_try_wait(a, parity)) {
-  }
+  SpinGuard g;
+  while (!mbar_try_wait(a, parity)) g.tick("mbarrier", a, parity);
 }
 
 // ------------------------------------------------------------------ TMA
@@ -236,7 +270,9 @@ __device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t* bar, uint32_t pa
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
+  SpinGuard g;
   while (!ok) {
+    g.tick("cluster mbarrier", a, parity);
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"

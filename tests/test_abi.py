@@ -222,3 +222,12 @@ def test_binding_does_no_method_arithmetic():
             if isinstance(node, ast.Call) and isinstance(node.func, ast.Attribute):
                 if node.func.attr in banned_calls:
                     assert base_name(node.func.value) not in outputs, (f, node.lineno, ast.unparse(node))
+
+
+def test_debug_build_exports_the_same_symbols(L):
+    """liblce_debug.so (trapping spin-wait timeouts) is the same ABI."""
+    mod = __import__("__graft_entry__").load_build_module()
+    path = mod.build_debug()
+    dbg = ctypes.CDLL(path)
+    for n in header_functions():
+        assert hasattr(dbg, n), n

@@ -9,6 +9,7 @@ The oracle always consumes the exact bf16 values the GPU consumed.
 """
 
 import math
+import sys
 import os
 
 import numpy as np
@@ -1317,3 +1318,27 @@ def test_full_size_dweight_rows_and_every_lse(cuda_lib, name, path):
     # the rows that are labels carry the -h_i onehot term: check them on their own too
     lab = np.isin(J, y[rows])
     assert fro_rel(got[lab], o["dW_rows"][lab]) <= GRAD_TOL
+
+
+def test_debug_sync_build_runs_clean(cuda_lib):
+    """liblce_debug.so (-DLCE_DEBUG_SYNC: every device spin wait traps after
+    2 s instead of hanging, sm100.cuh SpinGuard) on the sanitizer workload
+    (every entry point and GEMM variant at small ragged shapes), the smoke
+    parity check and one full-size 1B fused + split step (K-lockstep on):
+    no wait may come near the deadline on a correct schedule."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dbg = os.path.join(root, "paper_2605_21442_b200", "liblce_debug.so")
+    if not os.path.exists(dbg):
+        pytest.fail("liblce_debug.so missing: run __graft_entry__.build()")
+    env = dict(os.environ, LCE_LIB_PATH=dbg)
+    r = subprocess.run([sys.executable, "-c", "import paper_2605_21442_b200._lib as L; print(L.LIB_PATH)"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.stdout.strip().endswith("liblce_debug.so"), r.stdout + r.stderr
+    for cmd in (["scripts/sanitize.py"], ["-c", "import __graft_entry__ as g; g.smoke()"],
+                ["scripts/one_step.py", "--config", "llama1b", "--path", "fused", "--steps", "1"],
+                ["scripts/one_step.py", "--config", "llama1b", "--path", "split", "--steps", "1"]):
+        r = subprocess.run([sys.executable, *cmd], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+        out = r.stdout + r.stderr
+        assert r.returncode == 0 and "timed out" not in out, (cmd, out[-2000:])
