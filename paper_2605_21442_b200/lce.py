@@ -439,20 +439,43 @@ class LinearCrossEntropyFusedFunction(torch.autograd.Function):
         return dh, dw, None, None, None, None
 
 
+def _flatten_drop_in(hidden, labels):
+    """The drop-in form of P:132 (the model's [..., D] hidden states and [...]
+    class indices of any integer dtype, as torch's cross_entropy takes them)
+    marshalled to the ABI's [N, D] / int32 [N]: a view of hidden (a copy if it
+    is not contiguous) and the labels narrowed to int32 -- values outside the
+    int32 range are clamped to an int32 value that is still out of [0, V) (or
+    negative), so the library's S0 range check flags them instead of wrapping."""
+    if hidden.dim() < 2 or tuple(labels.shape) != tuple(hidden.shape[:-1]):
+        raise ValueError(f"hidden [..., D] and labels [...] must agree: {tuple(hidden.shape)} vs {tuple(labels.shape)}")
+    if labels.dtype.is_floating_point or labels.dtype == torch.bool:
+        raise TypeError(f"labels must be an integer tensor, got {labels.dtype}")
+    h = hidden.reshape(-1, hidden.shape[-1])
+    y = labels.reshape(-1)
+    if y.dtype != torch.int32:
+        y = y.clamp(-(2 ** 31), 2 ** 31 - 1).to(torch.int32)
+    return h, y.contiguous()
+
+
 def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduction: str = "mean",
                          fused: bool = False, grad_scale: float = 1.0):
-    """loss = CE(hidden @ weight^T, labels) (P:166 LCE).  fused=True computes the
-    gradients in the forward call without the logit recompute (MEAN / SUM only),
-    for the upstream gradient `grad_scale`; when no gradient is needed
-    (torch.no_grad(), or neither hidden nor weight requires grad) it runs the
-    forward only."""
+    """loss = CE(hidden @ weight^T, labels) (P:166 LCE), a drop-in for
+    cross_entropy(hidden @ weight.T, labels) (P:132): hidden [..., D] bf16,
+    labels [...] of any integer dtype; reduction 'none' returns [...].
+    fused=True computes the gradients in the forward call without the logit
+    recompute (MEAN / SUM only), for the upstream gradient `grad_scale`; when
+    no gradient is needed (torch.no_grad(), or neither hidden nor weight
+    requires grad) it runs the forward only."""
+    lead = tuple(labels.shape)
+    hidden, labels = _flatten_drop_in(hidden, labels)
     if fused:
         if reduction == "none":
             raise ValueError("fused autograd needs a scalar loss (reduction 'mean' or 'sum')")
         if torch.is_grad_enabled() and (hidden.requires_grad or weight.requires_grad):
             return LinearCrossEntropyFusedFunction.apply(hidden, weight, labels, ignore_index, reduction, grad_scale)
         return forward(hidden, weight, labels, ignore_index=ignore_index, reduction=reduction)["loss"].reshape(())
-    return LinearCrossEntropyFunction.apply(hidden, weight, labels, ignore_index, reduction)
+    res = LinearCrossEntropyFunction.apply(hidden, weight, labels, ignore_index, reduction)
+    return res.reshape(lead) if reduction == "none" else res
 
 
 def debug_gemm(A: torch.Tensor, B: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool) -> torch.Tensor:

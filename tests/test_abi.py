@@ -231,3 +231,23 @@ def test_debug_build_exports_the_same_symbols(L):
     dbg = ctypes.CDLL(path)
     for n in header_functions():
         assert hasattr(dbg, n), n
+
+
+def test_drop_in_marshalling_on_host(L):
+    """linear_cross_entropy's drop-in form: [..., D] hidden and [...]
+    integer labels become [N, D] / int32 [N]; int64 labels outside the int32
+    range stay out of range (clamped) instead of wrapping; mismatches raise."""
+    import torch
+
+    from paper_2605_21442_b200.lce import _flatten_drop_in
+
+    h = torch.zeros(2, 3, 8, dtype=torch.bfloat16)
+    y = torch.tensor([[0, 1, -100], [2 ** 32 + 5, -(2 ** 40), 7]], dtype=torch.int64)
+    h2, y2 = _flatten_drop_in(h, y)
+    assert tuple(h2.shape) == (6, 8) and h2.data_ptr() == h.data_ptr()  # a view
+    assert y2.dtype == torch.int32 and y2.is_contiguous()
+    assert y2.tolist() == [0, 1, -100, 2 ** 31 - 1, -(2 ** 31), 7]
+    with pytest.raises(ValueError):
+        _flatten_drop_in(h, y[:, :2])
+    with pytest.raises(TypeError):
+        _flatten_drop_in(h, y.float())

@@ -664,6 +664,49 @@ def test_autograd_function(cuda_lib):
     assert fro_rel(w.grad.float().cpu().double().numpy(), o["dW"]) <= 2e-2  # dW rounded to bf16 for autograd
 
 
+@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+def test_drop_in_batched_int64_labels(cuda_lib, fused, reduction):
+    """P:132 drop-in: hidden [B, S, D], labels [B, S] int64 (torch's class-index
+    dtype), gradients through autograd into the [B, S, D] leaf; 'none' returns
+    [B, S]; an int64 label outside the int32 range is flagged, not wrapped."""
+    import paper_2605_21442_b200 as F
+
+    if fused and reduction == "none":
+        pytest.skip("fused autograd needs a scalar loss")
+    B, S, D, V = 2, 150, 64, 1000
+    inp = small(B * S, D, V, seed=21)
+    h = inp.hidden.reshape(B, S, D).clone().requires_grad_(True)
+    w = inp.weight.clone().requires_grad_(True)
+    y64 = inp.labels.reshape(B, S).long()
+    loss = F.linear_cross_entropy(h, w, y64, reduction=reduction, fused=fused)
+    g = torch.linspace(-1, 1, B * S, device="cuda").reshape(B, S) if reduction == "none" else None
+    (loss * g).sum().backward() if g is not None else loss.backward()
+    torch.cuda.synchronize()
+    H, W, y = np_inputs(inp)
+    f = lce_forward(H, W, y, reduction=reduction)
+    gb = g.reshape(-1).double().cpu().numpy() if g is not None else 1.0
+    b = lce_backward(H, W, y, reduction=reduction, grad_loss=gb)
+    if reduction == "none":
+        assert tuple(loss.shape) == (B, S)
+        tok = loss.detach().reshape(-1).double().cpu().numpy()
+        assert np.abs(tok - f["token_loss"]).max() <= LSE_TOL * np.abs(f["lse"]).max()
+    else:
+        assert abs(loss.item() - f["loss"]) <= LOSS_TOL * abs(f["loss"])
+    assert tuple(h.grad.shape) == (B, S, D)
+    assert fro_rel(h.grad.reshape(-1, D).float().cpu().double().numpy(), b["dH"]) <= GRAD_TOL
+    assert fro_rel(w.grad.float().cpu().double().numpy(), b["dW"]) <= 2e-2  # bf16 dW for a bf16 leaf
+    if reduction == "mean" and not fused:
+        bad = y64.clone()
+        bad[0, 3] = 2 ** 32 + 5  # would wrap to 5 as a plain int32 cast
+        with torch.no_grad():
+            out = F.linear_cross_entropy(h.detach(), w.detach(), bad)
+        assert math.isnan(out.item())
+        with pytest.raises(F.LceError) as e:
+            F.check_device_status(device=h.device)
+        assert e.value.code == 6
+
+
 @pytest.mark.parametrize("N,D,V", [(300, 128, 3000), (257, 4096, 128256)])
 def test_none_reduction_per_token_logprobs(cuda_lib, variant, N, D, V):
     """R21 (GRPO / DPO token log-probs): per-token losses and
