@@ -10,6 +10,7 @@ from .lce import (  # noqa: F401
     Comm,
     LinearCrossEntropyFunction,
     LinearCrossEntropyFusedFunction,
+    LinearCrossEntropyLoss,
     Workspace,
     backward,
     backward_adamw,

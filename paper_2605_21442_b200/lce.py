@@ -478,6 +478,35 @@ def linear_cross_entropy(hidden, weight, labels, ignore_index: int = -100, reduc
     return res.reshape(lead) if reduction == "none" else res
 
 
+class LinearCrossEntropyLoss(torch.nn.Module):
+    """nn.Module form of the loss the paper names (torchtune's
+    LinearCrossEntropyLoss): holds the output projection (a weight
+    Parameter [V, D] or an nn.Linear without bias, e.g. the model's LM head)
+    and computes CE(hidden @ weight^T, labels) through linear_cross_entropy,
+    never materialising the [..., V] logits."""
+
+    def __init__(self, projection=None, ignore_index: int = -100, reduction: str = "mean", fused: bool = False):
+        super().__init__()
+        if reduction not in _RED:
+            raise ValueError(f"reduction must be 'mean', 'sum' or 'none', got {reduction!r}")
+        self.projection = projection
+        self.ignore_index, self.reduction, self.fused = ignore_index, reduction, fused
+
+    def _weight(self, weight):
+        w = weight if weight is not None else self.projection
+        if isinstance(w, torch.nn.Linear):
+            if w.bias is not None:
+                raise ValueError("the LCE projection has no bias (P:166: logits = hidden @ weight^T)")
+            w = w.weight
+        if w is None:
+            raise ValueError("no output projection: pass one to the constructor or to forward()")
+        return w
+
+    def forward(self, hidden, labels, weight=None, grad_scale: float = 1.0):
+        return linear_cross_entropy(hidden, self._weight(weight), labels, ignore_index=self.ignore_index,
+                                    reduction=self.reduction, fused=self.fused, grad_scale=grad_scale)
+
+
 def debug_gemm(A: torch.Tensor, B: torch.Tensor, M: int, N: int, K: int, a_mn: bool, b_mn: bool) -> torch.Tensor:
     """C = A B^T through the tcgen05 mainloop (diagnostics)."""
     C = torch.empty(M, N, dtype=torch.float32, device=A.device)

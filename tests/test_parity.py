@@ -707,6 +707,27 @@ def test_drop_in_batched_int64_labels(cuda_lib, fused, reduction):
         assert e.value.code == 6
 
 
+def test_loss_module_with_lm_head(cuda_lib):
+    """LinearCrossEntropyLoss (the paper's module name) around a bias-free
+    nn.Linear LM head: same loss and gradients as the oracle."""
+    import paper_2605_21442_b200 as F
+
+    B, S, D, V = 3, 100, 64, 1000
+    inp = small(B * S, D, V, seed=23)
+    head = torch.nn.Linear(D, V, bias=False, device="cuda", dtype=torch.bfloat16)
+    with torch.no_grad():
+        head.weight.copy_(inp.weight)
+    h = inp.hidden.reshape(B, S, D).clone().requires_grad_(True)
+    loss = F.LinearCrossEntropyLoss(head)(h, inp.labels.reshape(B, S).long())
+    loss.backward()
+    o = oracle_run(inp)
+    assert abs(loss.item() - o["loss"]) <= LOSS_TOL * abs(o["loss"])
+    assert fro_rel(h.grad.reshape(-1, D).float().cpu().double().numpy(), o["dH"]) <= GRAD_TOL
+    assert fro_rel(head.weight.grad.float().cpu().double().numpy(), o["dW"]) <= 2e-2
+    with pytest.raises(ValueError):
+        F.LinearCrossEntropyLoss(torch.nn.Linear(D, V, device="cuda", dtype=torch.bfloat16))(h, inp.labels.reshape(B, S))
+
+
 @pytest.mark.parametrize("N,D,V", [(300, 128, 3000), (257, 4096, 128256)])
 def test_none_reduction_per_token_logprobs(cuda_lib, variant, N, D, V):
     """R21 (GRPO / DPO token log-probs): per-token losses and
