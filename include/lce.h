@@ -124,8 +124,10 @@ typedef struct {
                                  [512 MiB, 4 GiB] and never below 4096 columns;
                                  lce_forward_backward: 2 GiB of bf16 q/G rows,
                                  or ceil(N/2) rows (two chunks) when those
-                                 take at most 4 GiB; KD: 4 GiB.  A
-                                 performance knob only.                          */
+                                 take at most 4 GiB; the chunk's N_c x D row
+                                 buffers (8 bytes per element) are bounded by
+                                 the same budget; KD: 4 GiB.  A performance
+                                 knob only.                                      */
 } lce_problem_t;
 
 /* Bytes of caller-provided device workspace both lce_forward and lce_backward

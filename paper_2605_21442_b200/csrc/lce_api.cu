@@ -214,6 +214,14 @@ bool make_fused_plan(const lce_problem_t* p, FusedPlan* fp, bool kd = false) {
     if (half > budget && half <= kTwoChunkBudget) budget = half;
   }
   int64_t nc_max = (budget / (per_elem * q.ldv)) / kPairBM * kPairBM;
+  // the chunk's row buffers that scale with N_c * D (H_c and the scaled H
+  // chunk in bf16, the vocab-parallel fp32 dH chunk: 8 bytes per element) stay
+  // within the budget as well -- only binding for small vocabularies (V_l <
+  // 4 D), where the q chunk alone would allow very tall chunks
+  if (!kd) {
+    const int64_t nc_rows = (budget / (8 * q.D)) / kPairBM * kPairBM;
+    if (nc_max > nc_rows) nc_max = nc_rows;
+  }
   if (nc_max < kPairBM) nc_max = kPairBM;
   if (nc_max > q.cap) nc_max = q.cap;
   // at least two row chunks: the chunk buffer never holds all N x V_l

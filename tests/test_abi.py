@@ -251,3 +251,14 @@ def test_drop_in_marshalling_on_host(L):
         _flatten_drop_in(h, y[:, :2])
     with pytest.raises(TypeError):
         _flatten_drop_in(h, y.float())
+
+
+def test_fused_row_buffers_bounded_for_small_vocab(L):
+    """Small vocabulary, many tokens (V = 1000, N = 2^20, D = 4096): the fused
+    chunk's N_c x D row buffers (H_c, scaled H, fp32 dH: 8 bytes per element)
+    stay within the 2 GiB budget, so the workspace is O(N) + budget-bounded
+    chunk buffers, not O(N/2 x D)."""
+    N, D, V = 1 << 20, 4096, 1000
+    w = L.lib.lce_fused_workspace_bytes(ctypes.byref(prob(L, N, D, V)))
+    per_row = 64  # index / label / lse / reference / factor sections: a few words per token
+    assert 0 < w < N * per_row + 3 * (2 << 30), w

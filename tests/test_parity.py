@@ -925,6 +925,16 @@ def test_fused_many_row_chunks_with_packed_labels(cuda_lib, variant):
     assert fro_rel(g["dW"], one["dW"]) <= 1e-5
 
 
+def test_fused_small_vocab_row_bound(cuda_lib):
+    """V_l < 4 D: the budget bounds the chunk by its N_c x D row buffers
+    (8 bytes per element), not by the q chunk: 512-row chunks here (the q
+    chunk alone would allow 1024), six chunks, dW accumulated over them."""
+    N, D, V = 3000, 256, 300
+    inp = small(N, D, V, seed=5)
+    g = fused_run(inp, budget=8 * D * 512)
+    assert_parity(g, oracle_run(inp), inp.labels.cpu().numpy())
+
+
 @pytest.mark.parametrize("n_valid", [511, 512, 513, 1024])
 def test_fused_default_plan_chunk_boundary(cuda_lib, n_valid):
     """Default (two-chunk) plan, N = 1024 -> 512-row chunks: the compacted
