@@ -184,19 +184,28 @@ struct TileInfo {
   int row;        // row of this thread inside the tile (== TMEM lane)
   bool zero_acc;  // empty k-range: the accumulator was never written, treat as 0
   int split;      // split-K index of this work item
-  uint8_t* smem;  // this warp's kEpiBufs x 4 KB epilogue staging tiles (1 KB aligned)
+  uint8_t* smem;  // this warp's nbufs x 4 KB epilogue staging tiles (1 KB aligned)
   uint32_t nst;   // TMA stores this warp has issued so far (selects the next staging tile)
   uint64_t st_policy;  // L2 cache policy for the epilogue's TMA stores
+  int nbufs;           // staging tiles of this warp (kEpiBufs; kWideEpiBufs in the wide kernel)
 };
 
 // This warp's next staging tile: waits (lane 0) until the store that last read
 // it is done reading, i.e. at most kEpiBufs - 1 newer stores may still be
 // reading.  Every call must be followed by exactly one committed store group.
 __device__ __forceinline__ uint8_t* stage_next(TileInfo& t) {
-  static_assert(kEpiBufs == 2, "wait depth below assumes two staging tiles");
-  if ((t.row & 31) == 0) tma_store_wait_read_1();
+  if ((t.row & 31) == 0) {
+    switch (t.nbufs) {  // the wait depth is an immediate
+      case 1: tma_store_wait_read_n<0>(); break;
+      case 2: tma_store_wait_read_n<1>(); break;
+      case 3: tma_store_wait_read_n<2>(); break;
+      case 4: tma_store_wait_read_n<3>(); break;
+      case 5: tma_store_wait_read_n<4>(); break;
+      default: tma_store_wait_read_n<5>(); break;
+    }
+  }
   __syncwarp();
-  uint8_t* st = t.smem + (t.nst & (kEpiBufs - 1)) * kEpiWarpSmem;
+  uint8_t* st = t.smem + (t.nst % static_cast<uint32_t>(t.nbufs)) * kEpiWarpSmem;
   ++t.nst;
   return st;
 }
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * BM, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
+                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp, kEpiBufs};
       Epi::prefetch(ep, ti);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -586,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int t = cluster; t < num_tiles; t += nclusters) {
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       TileInfo ti{w.mb * kPairBM + 128 * static_cast<int>(rank), w.nb * BN, w.nb, M, N, q * 32 + lane,
-                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
+                  w.kb1 == w.kb0, w.s, epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp, kEpiBufs};
       Epi::prefetch(ep, ti);
       mbar_wait_cluster(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -626,10 +635,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 // k-blocks hold ring stages the TMA needs for prefetch.)
 // =====================================================================
 constexpr int kWideBM = 512;  // rows per wide pair tile
-constexpr int kWideStages = 4;
+#ifndef LCE_WIDE_STAGES
+#define LCE_WIDE_STAGES 4
+#endif
+#ifndef LCE_WIDE_EPI_BUFS
+#define LCE_WIDE_EPI_BUFS 2
+#endif
+constexpr int kWideStages = LCE_WIDE_STAGES;
+// staging tiles per epilogue warp in the wide kernel: its unbuffered
+// accumulator is drained at every tile end, as fast as the TMA stores in
+// flight allow
+constexpr int kWideEpiBufs = LCE_WIDE_EPI_BUFS;
 constexpr int kWideAStage = 256 * BK * 2;  // 32 KB
 constexpr int kWideBStage = 128 * BK * 2;  // 16 KB
-constexpr int kWideSmemBytes = kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + kEpiSmemBytes;
+constexpr int kWideSmemBytes =
+    kWideStages * (kWideAStage + kWideBStage) + 1024 + 1024 + 4 * kWideEpiBufs * kEpiWarpSmem;
+static_assert(kWideSmemBytes <= 232448, "wide kernel exceeds 227 KB of shared memory");
 
 template <bool A_MN, bool B_MN, class Epi>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -814,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
       const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank);
       TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kEpiBufs * kEpiWarpSmem, nst, stp};
+                  epi_smem + q * kWideEpiBufs * kEpiWarpSmem, nst, stp, kWideEpiBufs};
       Epi::prefetch(ep, ti);
       ti.m0 = m0 + 128;
       Epi::prefetch(ep, ti);
