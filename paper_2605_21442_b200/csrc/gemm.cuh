@@ -82,8 +82,6 @@ struct GemmDims {
   unsigned long long* lock_prog;
   uint32_t lock_gen;
   int32_t lock_d;
-  // gemm_wide_phased_kernel: k-blocks each accumulator half runs alone at both tile ends
-  int32_t phase_r;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -829,272 +827,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    const int q = warp & 3;
-    uint32_t acc_phase = 0;
-    uint32_t nst = 0;
-    const uint64_t stp = l2_policy(dims.st_hint);
-    for (int t = cluster; t < num_tiles; t += nclusters) {
-      const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-      const int m0 = w.mb * kWideBM + 256 * static_cast<int>(rank);
-      TileInfo ti{m0, w.nb * BN, w.nb, M, N, q * 32 + lane, w.kb1 == w.kb0, w.s,
-                  epi_smem + q * kWideEpiBufs * kEpiWarpSmem, nst, stp, kWideEpiBufs};
-      Epi::prefetch(ep, ti);
-      ti.m0 = m0 + 128;
-      Epi::prefetch(ep, ti);
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        mbar_wait_cluster(&tfull[h], acc_phase);
-        tc_fence_after();
-        const uint32_t taddr = tmem_base + h * BN + (static_cast<uint32_t>(q * 32) << 16);
-        ti.m0 = m0 + 128 * h;
-        Epi::apply(ep, taddr, ti);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&tempty[h], 0);
-      }
-      nst = ti.nst;
-      acc_phase ^= 1;
-    }
-    Epi::finish(ep);
-  }
-
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  probe_mark(dims.probe, 2);
-  if (warp == 2) tmem_dealloc_pair(tmem_base, kTmemCols);
-}
-
-// =====================================================================
-// Phased wide variant (A/B only: LCE_WIDE_PHASED=1, dW): the 512 x 256 pair
-// tile of gemm_wide_kernel, scheduled so that each accumulator half's drain
-// overlaps MMAs of the other half.  A tile with nkb k-blocks is nkb + 2R steps
-// (R = min(phase_r, nkb / 2)):
-//   h0 alone on k-blocks [0, R)        (overlaps the drain of the previous tile's h1)
-//   h1 alone on k-blocks [0, R)        (B reloaded)
-//   both halves on [R, nkb - R)
-//   h0 alone on [nkb - R, nkb)         (h0 complete -> its drain starts)
-//   h1 alone on [nkb - R, nkb)         (overlaps h0's drain; B reloaded)
-// The operand ring is 12 slots of 16 KB (one A half or one B block each): a
-// two-half step takes 3 slots, a one-half step 2, so one-half steps keep about
-// 6 x 512 MMA cycles of loads in flight (the 4 x 48 KB ring held 4 x 512).
-// =====================================================================
-constexpr int kSlots = 12;
-constexpr int kSlotBytes = 128 * BK * 2;  // 16 KB
-constexpr int kPhasedSmemBytes = kSlots * kSlotBytes + 1024 + 1024 + 4 * kWideEpiBufs * kEpiWarpSmem;
-static_assert(kPhasedSmemBytes <= 232448, "phased wide kernel exceeds 227 KB of shared memory");
-
-struct PhaseStep {
-  int kb;    // k-block within the work item
-  int mask;  // accumulator halves: 1 = h0, 2 = h1, 3 = both
-};
-__device__ __forceinline__ PhaseStep phase_step(int i, int nkb, int R) {
-  if (i < R) return {i, 1};
-  if (i < 2 * R) return {i - R, 2};
-  const int mid = nkb - 2 * R;
-  if (i < 2 * R + mid) return {R + (i - 2 * R), 3};
-  const int j = i - 2 * R - mid;
-  return j < R ? PhaseStep{nkb - R + j, 1} : PhaseStep{nkb - R + (j - R), 2};
-}
-
-template <bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(kThreads, 1)
-    gemm_wide_phased_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            const GemmDims dims, const __grid_constant__ typename Epi::Params ep) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* slots = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(slots + kSlots * kSlotBytes);
-  uint64_t* empty = full + kSlots;
-  uint64_t* tfull = empty + kSlots;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  LockSmem* lsm = reinterpret_cast<LockSmem*>(tmem_slot + 4);
-  uint8_t* epi_smem = reinterpret_cast<uint8_t*>(full) + 1024;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int cluster = blockIdx.x >> 1;
-  const int nclusters = gridDim.x >> 1;
-
-  const int M = extent(dims.m_dev, dims.m_static, dims.m_off, dims.m_cap);
-  const int K = extent(dims.k_dev, dims.k_static, dims.k_off, dims.k_cap);
-  const int N = dims.n;
-  const int num_m = (M + kWideBM - 1) / kWideBM;
-  const int num_n = (N + BN - 1) / BN;
-  const int num_k = (K + BK - 1) / BK;
-  const int S = dims.ksplit > 1 ? dims.ksplit : 1;
-  const int GM = dims.group_m > 0 ? dims.group_m : kGroupM;
-  const int num_tiles = num_m * num_n * S;
-  const bool lock = dims.lock_prog != nullptr && leader && num_k > 0 && num_tiles > 0;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB);
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int h = 0; h < 2; ++h) {
-      mbar_init(&tfull[h], 1);
-      mbar_init(&tempty[h], 8);
-    }
-    lsm->steps = 0;
-    lsm->slowest = 0;
-    lsm->done = 0;
-    fence_mbar_init();
-  }
-  if (warp == 2) {
-    tmem_alloc_pair(tmem_slot, kTmemCols);
-    tmem_relinquish_pair();
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  probe_mark(dims.probe, 0);
-
-  if (warp == 0) {
-    if (lane == 0 && num_k > 0) {
-      // ---------------------------------------------------------- TMA producer (both CTAs)
-      int slot = 0;
-      uint32_t phase = 0;
-      auto next = [&]() {
-        if (++slot == kSlots) {
-          slot = 0;
-          phase ^= 1;
-        }
-      };
-      const uint64_t pa = l2_policy(dims.a_hint), pb = l2_policy(dims.b_hint);
-      uint32_t steps = 0;
-      bool lock_on = lock;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-        const int nkb = w.kb1 - w.kb0;
-        const int R = min(dims.phase_r, nkb / 2);
-        const int ma = w.mb * kWideBM + 256 * rank;
-        const int nbh = w.nb * BN + 128 * rank;
-        for (int i = 0; i < nkb + 2 * R; ++i) {
-          const PhaseStep ps = phase_step(i, nkb, R);
-          const int k0 = (w.kb0 + ps.kb) * BK;
-          if (lock) lockstep_gate(dims, lsm, steps++, lock_on);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            if (ps.mask & (1 << h)) {
-              mbar_wait(&empty[slot], phase ^ 1);
-              if (leader) mbar_arrive_expect_tx(&full[slot], 2 * kSlotBytes);
-              uint8_t* a = slots + slot * kSlotBytes;
-              if (!A_MN) {
-                tma_load_2d_pair(a, &tmA, &full[slot], k0, ma + 128 * h, pa);
-              } else {
-                tma_load_2d_pair(a, &tmA, &full[slot], ma + 128 * h, k0, pa);
-                tma_load_2d_pair(a + BK * 128, &tmA, &full[slot], ma + 128 * h + 64, k0, pa);
-              }
-              next();
-            }
-          }
-          mbar_wait(&empty[slot], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full[slot], 2 * kSlotBytes);
-          uint8_t* b = slots + slot * kSlotBytes;
-          if (!B_MN) {
-            tma_load_2d_pair(b, &tmB, &full[slot], k0, nbh, pb);
-          } else {
-            tma_load_2d_pair(b, &tmB, &full[slot], nbh, k0, pb);
-            tma_load_2d_pair(b + BK * 128, &tmB, &full[slot], nbh + 64, k0, pb);
-          }
-          next();
-        }
-      }
-      if (lock) lock_st(&lsm->done, 1u);
-    }
-  } else if (warp == 3) {
-    if (lock) lockstep_monitor(dims, lsm, cluster, nclusters, lane);
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ---------------------------------------------------------- MMA issuer (leader only)
-      constexpr uint32_t idesc = idesc_bf16_f32(kPairBM, BN, A_MN, B_MN);
-      int slot = 0;
-      uint32_t phase = 0;
-      uint32_t acc_phase = 0;
-      for (int t = cluster; t < num_tiles; t += nclusters) {
-        const WorkItem w = work_of(t, num_m, num_n, S, num_k, GM);
-        const int nkb = w.kb1 - w.kb0;
-        const int R = min(dims.phase_r, nkb / 2);
-        const int total = nkb + 2 * R;
-        // first / last step that uses each half in this tile
-        const int first1 = R > 0 ? R : 0;
-        const int last0 = R > 0 ? nkb + R - 1 : nkb - 1;
-        const int last1 = total - 1;
-        for (int i = 0; i < total; ++i) {
-          const PhaseStep ps = phase_step(i, nkb, R);
-          if (i == 0) {
-            mbar_wait_cluster(&tempty[0], acc_phase ^ 1);
-            tc_fence_after();
-          }
-          if (i == first1) {
-            mbar_wait_cluster(&tempty[1], acc_phase ^ 1);
-            tc_fence_after();
-          }
-          // slots of this step (A half 0, A half 1, B), in ring order; -1 = unused
-          int sa0 = -1, sa1 = -1;
-          if (ps.mask & 1) {
-            mbar_wait(&full[slot], phase);
-            sa0 = slot;
-            if (++slot == kSlots) {
-              slot = 0;
-              phase ^= 1;
-            }
-          }
-          if (ps.mask & 2) {
-            mbar_wait(&full[slot], phase);
-            sa1 = slot;
-            if (++slot == kSlots) {
-              slot = 0;
-              phase ^= 1;
-            }
-          }
-          mbar_wait(&full[slot], phase);
-          const int sb = slot;
-          if (++slot == kSlots) {
-            slot = 0;
-            phase ^= 1;
-          }
-          tc_fence_after();
-          const uint32_t b_addr = smem_u32(slots + sb * kSlotBytes);
-          auto issue = [&](int sa, int h, bool first) {
-            const uint32_t a_addr = smem_u32(slots + sa * kSlotBytes);
-            const uint32_t d = tmem_base + h * BN;
-#pragma unroll
-            for (int kk = 0; kk < BK / UK; ++kk) {
-              const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + kk * (UK * 128), BK * 128, 1024)
-                                       : smem_desc_sw128(a_addr + kk * (UK * 2), 16, 1024);
-              const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + kk * (UK * 128), BK * 128, 1024)
-                                       : smem_desc_sw128(b_addr + kk * (UK * 2), 16, 1024);
-              mma_bf16_ss_pair(d, ad, bd, idesc, (first && kk == 0) ? 0u : 1u);
-            }
-          };
-          if (sa0 >= 0) issue(sa0, 0, i == 0);
-          if (sa1 >= 0) issue(sa1, 1, i == first1);
-          if (sa0 >= 0) mma_commit_pair(&empty[sa0], 0x3);
-          if (sa1 >= 0) mma_commit_pair(&empty[sa1], 0x3);
-          mma_commit_pair(&empty[sb], 0x3);
-          if (i == last0) mma_commit_pair(&tfull[0], 0x3);
-          if (i == last1) mma_commit_pair(&tfull[1], 0x3);
-        }
-        if (nkb == 0) {  // empty k-range: the epilogue treats both halves as zero
-          for (int h = 0; h < 2; ++h) {
-            mbar_wait_cluster(&tempty[h], acc_phase ^ 1);
-            mbar_arrive_cluster(&tfull[h], 0);
-            mbar_arrive_cluster(&tfull[h], 1);
-          }
-        }
-        acc_phase ^= 1;
-      }
-    }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ epilogue (both CTAs), as gemm_wide_kernel
     const int q = warp & 3;
     uint32_t acc_phase = 0;
     uint32_t nst = 0;

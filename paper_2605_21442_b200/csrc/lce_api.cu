@@ -15,7 +15,6 @@
 #include <atomic>
 #include <mutex>
 #include <vector>
-#include <type_traits>
 
 #include "../../include/lce.h"
 #include "kernels.cuh"
@@ -376,8 +375,6 @@ lce_status_t device_info(DevInfo* out) {
     LCE_SMEM_ATTR(false, true, EpiDW);
     LCE_SMEM_ATTR(true, false, EpiDW);
 #undef LCE_SMEM_ATTR
-    LCE_CUDA(cudaFuncSetAttribute(gemm_wide_phased_kernel<true, true, EpiDW>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPhasedSmemBytes));
   }
   if (dev < 64) {
     cache[dev] = d;
@@ -672,22 +669,8 @@ lce_status_t launch_gemm(int cls, const CUtensorMap& a, const CUtensorMap& b, co
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (wide) cfg.dynamicSmemBytes = kWideSmemBytes;
-  cudaError_t e = cudaSuccess;
-  bool phased = false;
-  if constexpr (A_MN && B_MN && std::is_same<Epi, EpiDW>::value) {
-    // A/B: LCE_WIDE_PHASED=R runs the wide dW tiles on the phased schedule
-    // (gemm_wide_phased_kernel: each half alone on R k-blocks at both tile ends)
-    const char* ph = getenv("LCE_WIDE_PHASED");
-    if (wide && ph && *ph && atoi(ph) >= 0) {
-      d.phase_r = atoi(ph);
-      cfg.dynamicSmemBytes = kPhasedSmemBytes;
-      e = cudaLaunchKernelEx(&cfg, gemm_wide_phased_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
-      phased = true;
-    }
-  }
-  if (!phased)
-    e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
-             : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
+  cudaError_t e = wide ? cudaLaunchKernelEx(&cfg, gemm_wide_kernel<A_MN, B_MN, Epi>, a, b, d, ep)
+                       : cudaLaunchKernelEx(&cfg, gemm_pair_kernel<A_MN, B_MN, Epi>, a, b, d, ep);
   if (e != cudaSuccess) {
     if (getenv("LCE_DEBUG")) fprintf(stderr, "lce: cudaLaunchKernelEx -> %s\n", cudaGetErrorString(e));
     return LCE_ERR_CUDA;
