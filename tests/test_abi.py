@@ -262,3 +262,15 @@ def test_fused_row_buffers_bounded_for_small_vocab(L):
     w = L.lib.lce_fused_workspace_bytes(ctypes.byref(prob(L, N, D, V)))
     per_row = 64  # index / label / lse / reference / factor sections: a few words per token
     assert 0 < w < N * per_row + 3 * (2 << 30), w
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No liblce.so -> importing the package raises; there is nothing to fall back to."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, LCE_LIB_PATH=str(tmp_path / "no_such_liblce.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2605_21442_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "liblce" in (r.stderr + r.stdout)
